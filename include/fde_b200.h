@@ -1,0 +1,220 @@
+/* fde_b200.h -- C ABI of the B200-native CN-WSGD time-step solver.
+ *
+ * Drop-in boundary for the reference hot path (arXiv 1706.06844 reference,
+ * /root/reference/proj).  Each entry point names the reference interface it
+ * replaces (file:line under proj/).  Plain pointers and sizes only; every
+ * function returns an fde_status, and fde_last_error() holds the message of
+ * the last failure on the calling thread.
+ *
+ * Memory: vectors passed to fde_op_*, fde_mg_*, fde_precond_*, fde_gmres and
+ * fde_bicgstab are DEVICE pointers (cudaMalloc'd, FP64, x index fastest:
+ * p = i + j*n1, proj/src/problem.cpp:59).  fde_march_* and fde_time_march
+ * take HOST arrays (the reference time_march signature) and do the copies.
+ * Streams are cudaStream_t passed as void* (NULL = legacy default stream).
+ * Handles own their device memory; operations on one handle are ordered on
+ * the stream given and are not re-entrant across streams.
+ * There is no CPU fallback: without a usable CUDA device every call that
+ * touches the device fails with FDE_ECUDA.
+ */
+#ifndef FDE_B200_H
+#define FDE_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FDE_OK = 0,
+  FDE_EINVAL = 1,   /* std::invalid_argument in the reference (sizes, gamma, signs, diagonal) */
+  FDE_ERUNTIME = 2, /* std::runtime_error in the reference (singular factorisation) */
+  FDE_ECUDA = 3,    /* CUDA runtime failure */
+  FDE_ENOMEM = 4
+} fde_status;
+
+const char* fde_last_error(void);
+int fde_abi_version(void); /* FDE_B200_ABI_VERSION */
+#define FDE_B200_ABI_VERSION 1
+
+/* ---------------------------------------------------------------- weights
+ * binom_coeffs + wsgd_weights (proj/include/fde/weights.hpp:14-25,
+ * proj/src/weights.cpp:21-51).  pq = 0: WSGD (p,q) = (1,0) (the reference);
+ * pq = 1: (1,-1) (BASELINE cfg3 extension, not in the reference).
+ * g and w receive K+1 values. */
+int fde_wsgd_weights(double gamma, size_t K, int pq, double* g, double* w);
+
+/* ----------------------------------------------- structured operator
+ * StructuredFdeOperator (proj/include/fde/structured.hpp:57-97) built from
+ * ToeplitzBlock(first_col, first_row) pairs (structured.hpp:22) and the four
+ * diagonal coefficient fields (host arrays, n1*n2 each). */
+typedef struct fde_op_s* fde_op;
+int fde_op_create(size_t n1, size_t n2, double inv_r, double s_over_r, const double* col_x,
+                  const double* row_x, const double* col_y, const double* row_y,
+                  const double* dp, const double* dm, const double* ep, const double* em,
+                  fde_op* out);
+/* Same with ToeplitzBlock::fractional blocks (structured.cpp:47-55). */
+int fde_op_create_fractional(size_t n1, size_t n2, double inv_r, double s_over_r,
+                             double alpha, double beta, int pq, const double* dp,
+                             const double* dm, const double* ep, const double* em,
+                             fde_op* out);
+int fde_op_size(fde_op op, size_t* n);
+/* LinOp::apply (proj/include/fde/linop.hpp:13): y = M x */
+int fde_op_apply(fde_op op, const double* x, double* y, void* stream);
+/* StructuredFdeOperator::apply_rhs (structured.hpp:86): structured terms negated */
+int fde_op_apply_rhs(fde_op op, const double* x, double* y, void* stream);
+/* LinOp::diagonal (linop.hpp:14): copies the diagonal to host array d (n values) */
+int fde_op_diagonal(fde_op op, double* d);
+/* StructuredFdeOperator::scale (structured.hpp:91) */
+int fde_op_scale(fde_op op, double s);
+int fde_op_destroy(fde_op op);
+
+/* ---------------------------------------------------------- the problem
+ * FdeProblem (proj/include/fde/problem.hpp:22-33) with C callbacks in place
+ * of std::function.  ctx is passed back to every callback. */
+typedef double (*fde_field_fn)(double x, double y, double t, void* ctx);
+typedef double (*fde_initial_fn)(double x, double y, void* ctx);
+typedef struct {
+  double alpha, beta;
+  double ax, bx, ay, by;
+  double t_final;
+  int time_dependent_coeffs; /* must be 0: time-dependent coefficients are not supported yet */
+  int pq;                    /* 0 = (1,0) reference weights, 1 = (1,-1) */
+  fde_field_fn d_plus, d_minus, e_plus, e_minus, source;
+  fde_initial_fn initial;
+  void* ctx;
+  /* BASELINE preset id (1..5) or 0 for a custom problem.  Presets evaluate
+   * coefficients/sources natively (fde_problem_preset fills this struct). */
+  int preset;
+  int source_kind; /* presets: 0 U[0,1), 1 1e-2 N(0,1), 2 zero */
+  unsigned long long seed;
+} fde_problem;
+
+/* The five BASELINE configurations; steps = 0 / tau <= 0 /
+ * source_kind < 0 select the config defaults.  Writes n (grid size per
+ * direction) and steps to *n_out / *steps_out when non-NULL. */
+int fde_problem_preset(int cfg, unsigned long long seed, int source_kind, size_t steps,
+                       double tau, fde_problem* out, size_t* n_out, size_t* steps_out);
+/* Grid (problem.cpp:27-48): out[5] = {hx, hy, dt, inv_r, s_over_r} */
+int fde_grid(const fde_problem* p, size_t n1, size_t n2, size_t steps, double* out);
+/* assemble_step_operator (problem.hpp:54-55) */
+int fde_assemble_step_operator(const fde_problem* p, size_t n1, size_t n2, size_t steps,
+                               size_t m, fde_op* out);
+/* sample_initial / source samples v(x_i, y_j, t^{m-1/2}) to host arrays */
+int fde_sample_initial(const fde_problem* p, size_t n1, size_t n2, size_t steps, double* u);
+int fde_sample_source(const fde_problem* p, size_t n1, size_t n2, size_t steps, size_t m,
+                      double* v);
+
+/* ---------------------------------------------------------- multigrid
+ * mg::plan_level_dims (proj/include/fde/multigrid.hpp:39-40): dims receives
+ * n_levels (n1, n2) pairs (at most max_levels). */
+int fde_plan_level_dims(size_t n1, size_t n2, double ratio0, double alpha, double beta,
+                        size_t* dims, size_t max_levels, size_t* n_levels);
+/* mg::anisotropy_ratio (multigrid.hpp:28-29) */
+int fde_anisotropy_ratio(fde_op op, double alpha, double beta, double* ratio);
+/* GridTransfer (multigrid.hpp:50-77), device arrays:
+ * op 0 prolong (coarse -> fine), 1 restrict_full, 2 restrict_transpose. */
+int fde_transfer(size_t n1, size_t n2, int coarsen_x, int coarsen_y, int op, const double* in,
+                 double* out, void* stream);
+
+typedef struct fde_mg_s* fde_mg;
+/* CoarseSolve (multigrid.hpp:95): 0 lu, 1 sweeps, 2 none */
+/* build_geometric_hierarchy (multigrid.hpp:141-144) */
+int fde_mg_build_geometric(const fde_problem* p, size_t n1, size_t n2, size_t steps, size_t m,
+                           double omega, int coarse, size_t coarse_sweeps, fde_mg* out);
+/* MgHierarchy(levels, geometric, ...) from caller-built level operators
+ * (multigrid.hpp:109-111); the handles are retained by the hierarchy. */
+int fde_mg_create(const fde_op* levels, size_t n_levels, double omega, int coarse,
+                  size_t coarse_sweeps, fde_mg* out);
+/* Galerkin hierarchy of the banded P2 companion (P2VcyclePrecond,
+ * proj/src/precond.cpp:75-83) */
+int fde_mg_build_p2(fde_op fine, double omega, fde_mg* out);
+int fde_mg_depth(fde_mg h, size_t* depth);
+int fde_mg_level_dims(fde_mg h, size_t level, size_t* n1, size_t* n2);
+/* MgHierarchy::vcycle (multigrid.hpp:119): x is the initial guess, updated.
+ * zero_guess != 0 asserts x == 0 (the reference scans for it). */
+int fde_mg_vcycle(fde_mg h, const double* b, double* x, int zero_guess, void* stream);
+int fde_mg_destroy(fde_mg h);
+
+/* ------------------------------------------------------ preconditioner
+ * make_preconditioner (proj/include/fde/precond.hpp:94-98): kind 0 none,
+ * 1 p2 (banded Galerkin V-cycle), 2 mgm (geometric V-cycle). */
+typedef struct fde_precond_s* fde_precond;
+int fde_precond_create(int kind, const fde_problem* p, size_t n1, size_t n2, size_t steps,
+                       size_t m, fde_op op, double omega, size_t cycles, int coarse,
+                       size_t coarse_sweeps, fde_precond* out);
+/* Precond::apply (krylov.hpp:11-14): z = M^-1 r */
+int fde_precond_apply(fde_precond pc, const double* r, double* z, void* stream);
+int fde_precond_destroy(fde_precond pc);
+
+/* --------------------------------------------------------------- Krylov
+ * SolverConfig / KrylovResult (proj/include/fde/krylov.hpp:16-30). */
+typedef struct {
+  double tol;
+  size_t restart;
+  size_t max_outer;
+} fde_solver_config;
+typedef struct {
+  size_t total_iterations;
+  int converged;
+  size_t n_history;        /* entries written to history (<= history_capacity) */
+  size_t history_length;   /* full length of residual_history */
+  double* history;         /* caller buffer, may be NULL */
+  size_t history_capacity;
+} fde_krylov_result;
+/* gmres (krylov.hpp:38-40), zero initial guess; x (device) receives the solution. */
+int fde_gmres(fde_op a, fde_precond m, const fde_solver_config* cfg, const double* b,
+              double* x, fde_krylov_result* res, void* stream);
+/* Left-preconditioned BiCGSTAB with the gmres stopping rule (extension; max
+ * iterations = restart * max_outer). */
+int fde_bicgstab(fde_op a, fde_precond m, const fde_solver_config* cfg, const double* b,
+                 double* x, fde_krylov_result* res, void* stream);
+
+/* ----------------------------------------------------------- time march
+ * DriverConfig (proj/include/fde/driver.hpp:12-21) + solver choice. */
+typedef struct {
+  int precond;          /* 0 none, 1 p2, 2 mgm */
+  double tol;
+  size_t restart;
+  size_t max_outer;
+  double omega;
+  size_t cycles;
+  int coarse;           /* 0 lu, 1 sweeps, 2 none */
+  size_t coarse_sweeps;
+  int solver;           /* 0 gmres (reference), 1 bicgstab (extension) */
+} fde_driver_config;
+void fde_driver_config_default(fde_driver_config* cfg); /* reference defaults */
+
+typedef struct fde_march_s* fde_march;
+/* Set-up half of time_march (driver.cpp:20-33): u0, step operator and
+ * preconditioner resident on the device. */
+int fde_march_create(const fde_problem* p, size_t n1, size_t n2, size_t steps,
+                     const fde_driver_config* cfg, fde_march* out);
+/* One time step m (driver.cpp:34-52): b = apply_rhs(u) + 2 hx^alpha v, GMRES
+ * from zero, u <- solution.  source: v(x_i, y_j, t^{m-1/2}) as
+ *   source_mode 0: evaluated by the library (problem callback or preset),
+ *   source_mode 1: HOST array (copied to the device inside the call),
+ *   source_mode 2: DEVICE array. */
+int fde_march_step(fde_march h, const double* source, int source_mode, void* stream,
+                   size_t* iterations, double* residual);
+/* Current step index m (steps taken so far) */
+int fde_march_steps_taken(fde_march h, size_t* m);
+/* u^m to a host (to_host != 0) or device array */
+int fde_march_solution(fde_march h, double* u, int to_host, void* stream);
+/* Device pointer of u^m (valid until the next step) */
+int fde_march_solution_ptr(fde_march h, const double** u_dev);
+int fde_march_destroy(fde_march h);
+
+/* time_march (proj/include/fde/driver.hpp:39-40): all steps, host outputs.
+ * step_iterations / step_residuals hold `steps` entries; solution n1*n2. */
+int fde_time_march(const fde_problem* p, size_t n1, size_t n2, size_t steps,
+                   const fde_driver_config* cfg, double* solution, size_t* step_iterations,
+                   double* step_residuals, double* wall_seconds);
+
+/* Number of kernels this library has launched since load (instrumentation). */
+unsigned long long fde_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDE_B200_H */

@@ -1,0 +1,578 @@
+// extern "C" boundary (include/fde_b200.h) over the B200 host classes.
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "../../include/fde_b200.h"
+#include "krylov.cuh"
+#include "problem.cuh"
+
+namespace fde_b200 {
+std::atomic<unsigned long long> g_kernel_launches{0};
+}
+
+using namespace fde_b200;
+
+struct fde_op_s {
+  std::shared_ptr<StructuredOp> op;
+  std::unique_ptr<KrylovWorkspace> ws;  // reused by fde_gmres / fde_bicgstab
+};
+struct fde_mg_s {
+  std::shared_ptr<Hierarchy> h;
+};
+struct fde_precond_s {
+  std::shared_ptr<Precond> pc;
+};
+struct fde_march_s {
+  Problem p;
+  Grid g;
+  fde_driver_config cfg;
+  std::shared_ptr<StructuredOp> op;
+  std::shared_ptr<Precond> pc;
+  std::unique_ptr<KrylovWorkspace> ws;
+  DevBuf<double> u, b, src, x;
+  std::vector<double> host_src;
+  double scale = 0.0;  // 2 hx^alpha (problem.cpp:82)
+  size_t m = 0;
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return FDE_OK;
+  } catch (const InvalidArgument& e) {
+    g_error = e.what();
+    return FDE_EINVAL;
+  } catch (const RuntimeError& e) {
+    g_error = e.what();
+    return FDE_ERUNTIME;
+  } catch (const CudaError& e) {
+    g_error = e.what();
+    return FDE_ECUDA;
+  } catch (const std::bad_alloc&) {
+    g_error = "out of host memory";
+    return FDE_ENOMEM;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return FDE_ERUNTIME;
+  }
+}
+
+void need(bool ok, const char* what) {
+  if (!ok) throw InvalidArgument(what);
+}
+
+cudaStream_t stream_of(void* s) { return static_cast<cudaStream_t>(s); }
+
+// fde_problem (C callbacks or preset) -> Problem
+Problem to_problem(const fde_problem* c) {
+  need(c != nullptr, "null problem");
+  need(!c->time_dependent_coeffs,
+       "time-dependent coefficients are not supported by this build (SURVEY 8(f) next)");
+  Problem p;
+  if (c->preset) {
+    p = make_preset(c->preset, c->seed, c->source_kind, 0, 0.0);
+  } else {
+    need(c->d_plus && c->d_minus && c->e_plus && c->e_minus, "problem is missing a coefficient field");
+    void* ctx = c->ctx;
+    auto wrap3 = [ctx](fde_field_fn f) {
+      return std::function<double(double, double, double)>(
+          [f, ctx](double x, double y, double t) { return f(x, y, t, ctx); });
+    };
+    p.d_plus = wrap3(c->d_plus);
+    p.d_minus = wrap3(c->d_minus);
+    p.e_plus = wrap3(c->e_plus);
+    p.e_minus = wrap3(c->e_minus);
+    if (c->source) p.source = wrap3(c->source);
+    if (c->initial) {
+      fde_initial_fn f = c->initial;
+      p.initial = [f, ctx](double x, double y) { return f(x, y, ctx); };
+    }
+  }
+  p.alpha = c->alpha;
+  p.beta = c->beta;
+  p.ax = c->ax;
+  p.bx = c->bx;
+  p.ay = c->ay;
+  p.by = c->by;
+  p.t_final = c->t_final;
+  p.pq = c->pq;
+  need(p.pq == 0 || p.pq == 1, "pq must be 0 ((1,0)) or 1 ((1,-1))");
+  return p;
+}
+
+void fill_result(const KrylovResult& r, fde_krylov_result* out) {
+  if (!out) return;
+  out->total_iterations = r.total_iterations;
+  out->converged = r.converged ? 1 : 0;
+  out->history_length = r.residual_history.size();
+  size_t nh = r.residual_history.size();
+  if (!out->history) nh = 0;
+  if (nh > out->history_capacity) nh = out->history_capacity;
+  for (size_t k = 0; k < nh; ++k) out->history[k] = r.residual_history[k];
+  out->n_history = nh;
+}
+
+std::shared_ptr<Precond> make_pc(int kind, const Problem& p, const Grid& g, size_t m,
+                                 const std::shared_ptr<StructuredOp>& op, double omega,
+                                 size_t cycles, int coarse, size_t sweeps) {
+  switch (kind) {  // make_preconditioner, precond.cpp:135-157
+    case PC_NONE:
+      return std::make_shared<Precond>(PC_NONE, nullptr, op->size(), 1);
+    case PC_P2:
+      return std::make_shared<Precond>(PC_P2, build_p2_hierarchy(*op, omega), op->size(), cycles);
+    case PC_MGM:
+      return std::make_shared<Precond>(
+          PC_MGM, build_geometric_hierarchy(p, g, m, omega, coarse, sweeps), op->size(), cycles);
+  }
+  throw InvalidArgument("unknown preconditioner kind");
+}
+
+KrylovWorkspace& workspace_for(std::unique_ptr<KrylovWorkspace>& ws, size_t n, size_t restart) {
+  const size_t need_rst = restart < 5 ? 5 : restart;
+  if (!ws || ws->n() != n || ws->restart() < need_rst)
+    ws = std::make_unique<KrylovWorkspace>(n, need_rst);
+  return *ws;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fde_last_error(void) { return g_error.c_str(); }
+int fde_abi_version(void) { return FDE_B200_ABI_VERSION; }
+unsigned long long fde_kernel_launches(void) { return g_kernel_launches.load(); }
+
+int fde_wsgd_weights(double gamma, size_t K, int pq, double* g, double* w) {
+  return guard([&] {
+    need(g && w, "null output");
+    const auto gg = binom_coeffs(gamma, K);
+    const auto ww = wsgd_weights(gamma, K, pq);
+    std::memcpy(g, gg.data(), gg.size() * sizeof(double));
+    std::memcpy(w, ww.data(), ww.size() * sizeof(double));
+  });
+}
+
+int fde_op_create(size_t n1, size_t n2, double inv_r, double s_over_r, const double* col_x,
+                  const double* row_x, const double* col_y, const double* row_y,
+                  const double* dp, const double* dm, const double* ep, const double* em,
+                  fde_op* out) {
+  return guard([&] {
+    need(out && col_x && row_x && col_y && row_y && dp && dm && ep && em, "null argument");
+    const size_t n = n1 * n2;
+    auto h = std::make_unique<fde_op_s>();
+    h->op = std::make_shared<StructuredOp>(
+        n1, n2, inv_r, s_over_r, ToeplitzDev({col_x, col_x + n1}, {row_x, row_x + n1}),
+        ToeplitzDev({col_y, col_y + n2}, {row_y, row_y + n2}), std::vector<double>(dp, dp + n),
+        std::vector<double>(dm, dm + n), std::vector<double>(ep, ep + n),
+        std::vector<double>(em, em + n));
+    *out = h.release();
+  });
+}
+
+int fde_op_create_fractional(size_t n1, size_t n2, double inv_r, double s_over_r,
+                             double alpha, double beta, int pq, const double* dp,
+                             const double* dm, const double* ep, const double* em,
+                             fde_op* out) {
+  return guard([&] {
+    need(out && dp && dm && ep && em, "null argument");
+    const size_t n = n1 * n2;
+    auto h = std::make_unique<fde_op_s>();
+    h->op = std::make_shared<StructuredOp>(
+        n1, n2, inv_r, s_over_r, ToeplitzDev::fractional(alpha, n1, pq),
+        ToeplitzDev::fractional(beta, n2, pq), std::vector<double>(dp, dp + n),
+        std::vector<double>(dm, dm + n), std::vector<double>(ep, ep + n),
+        std::vector<double>(em, em + n));
+    *out = h.release();
+  });
+}
+
+int fde_op_size(fde_op op, size_t* n) {
+  return guard([&] {
+    need(op && n, "null argument");
+    *n = op->op->size();
+  });
+}
+int fde_op_apply(fde_op op, const double* x, double* y, void* stream) {
+  return guard([&] {
+    need(op && x && y, "null argument");
+    need(x != y, "apply cannot run in place");
+    op->op->apply(x, y, stream_of(stream));
+  });
+}
+int fde_op_apply_rhs(fde_op op, const double* x, double* y, void* stream) {
+  return guard([&] {
+    need(op && x && y, "null argument");
+    need(x != y, "apply_rhs cannot run in place");
+    op->op->apply_rhs(x, y, stream_of(stream));
+  });
+}
+int fde_op_diagonal(fde_op op, double* d) {
+  return guard([&] {
+    need(op && d, "null argument");
+    const auto& v = op->op->diagonal();
+    std::memcpy(d, v.data(), v.size() * sizeof(double));
+  });
+}
+int fde_op_scale(fde_op op, double s) {
+  return guard([&] {
+    need(op != nullptr, "null argument");
+    op->op->scale(s);
+  });
+}
+int fde_op_destroy(fde_op op) {
+  return guard([&] { delete op; });
+}
+
+int fde_problem_preset(int cfg, unsigned long long seed, int source_kind, size_t steps,
+                       double tau, fde_problem* out, size_t* n_out, size_t* steps_out) {
+  return guard([&] {
+    need(out != nullptr, "null output");
+    const PresetInfo in = preset_info(cfg);
+    const size_t st = steps ? steps : in.steps;
+    std::memset(out, 0, sizeof *out);
+    out->alpha = in.alpha;
+    out->beta = in.beta;
+    out->ax = 0.0;
+    out->bx = 1.0;
+    out->ay = 0.0;
+    out->by = 1.0;
+    out->t_final = (tau > 0 ? tau : in.tau) * static_cast<double>(st);
+    out->pq = in.pq;
+    out->preset = cfg;
+    out->source_kind = source_kind >= 0 ? source_kind : in.source_kind;
+    out->seed = seed;
+    if (n_out) *n_out = in.n;
+    if (steps_out) *steps_out = st;
+  });
+}
+
+int fde_grid(const fde_problem* p, size_t n1, size_t n2, size_t steps, double* out) {
+  return guard([&] {
+    need(out != nullptr, "null output");
+    const Grid g(to_problem(p), n1, n2, steps);
+    out[0] = g.hx;
+    out[1] = g.hy;
+    out[2] = g.dt;
+    out[3] = g.inv_r;
+    out[4] = g.s_over_r;
+  });
+}
+
+int fde_assemble_step_operator(const fde_problem* p, size_t n1, size_t n2, size_t steps,
+                               size_t m, fde_op* out) {
+  return guard([&] {
+    need(out != nullptr, "null output");
+    const Problem pr = to_problem(p);
+    const Grid g(pr, n1, n2, steps);
+    auto h = std::make_unique<fde_op_s>();
+    h->op = assemble_step_operator(pr, g, m);
+    *out = h.release();
+  });
+}
+
+int fde_sample_initial(const fde_problem* p, size_t n1, size_t n2, size_t steps, double* u) {
+  return guard([&] {
+    need(u != nullptr, "null output");
+    const Problem pr = to_problem(p);
+    const Grid g(pr, n1, n2, steps);
+    const auto v = sample_initial(pr, g);
+    std::memcpy(u, v.data(), v.size() * sizeof(double));
+  });
+}
+
+int fde_sample_source(const fde_problem* p, size_t n1, size_t n2, size_t steps, size_t m,
+                      double* v) {
+  return guard([&] {
+    need(v != nullptr, "null output");
+    need(m >= 1, "step index starts at 1");
+    const Problem pr = to_problem(p);
+    const Grid g(pr, n1, n2, steps);
+    sample_source(pr, g, m, v);
+  });
+}
+
+int fde_plan_level_dims(size_t n1, size_t n2, double ratio0, double alpha, double beta,
+                        size_t* dims, size_t max_levels, size_t* n_levels) {
+  return guard([&] {
+    need(dims && n_levels, "null output");
+    const auto d = plan_level_dims(n1, n2, ratio0, alpha, beta);
+    *n_levels = d.size();
+    for (size_t l = 0; l < d.size() && l < max_levels; ++l) {
+      dims[2 * l] = d[l].first;
+      dims[2 * l + 1] = d[l].second;
+    }
+  });
+}
+
+int fde_anisotropy_ratio(fde_op op, double alpha, double beta, double* ratio) {
+  return guard([&] {
+    need(op && ratio, "null argument");
+    *ratio = anisotropy_ratio(*op->op, alpha, beta);
+  });
+}
+
+int fde_transfer(size_t n1, size_t n2, int coarsen_x, int coarsen_y, int op, const double* in,
+                 double* out, void* stream) {
+  return guard([&] {
+    need(in && out, "null argument");
+    const Xfer t = make_xfer((int)n1, (int)n2, coarsen_x != 0, coarsen_y != 0);
+    if (op == 0) xfer_prolong(t, in, out, stream_of(stream));
+    else if (op == 1) xfer_restrict(t, in, out, 0.5, stream_of(stream));
+    else if (op == 2) xfer_restrict(t, in, out, 1.0, stream_of(stream));
+    else throw InvalidArgument("transfer op must be 0, 1 or 2");
+  });
+}
+
+int fde_mg_build_geometric(const fde_problem* p, size_t n1, size_t n2, size_t steps, size_t m,
+                           double omega, int coarse, size_t coarse_sweeps, fde_mg* out) {
+  return guard([&] {
+    need(out != nullptr, "null output");
+    const Problem pr = to_problem(p);
+    const Grid g(pr, n1, n2, steps);
+    auto h = std::make_unique<fde_mg_s>();
+    h->h = build_geometric_hierarchy(pr, g, m, omega, coarse, coarse_sweeps);
+    *out = h.release();
+  });
+}
+
+int fde_mg_create(const fde_op* levels, size_t n_levels, double omega, int coarse,
+                  size_t coarse_sweeps, fde_mg* out) {
+  return guard([&] {
+    need(out && levels && n_levels > 0, "null argument");
+    std::vector<LevelOp> lv;
+    std::vector<std::pair<size_t, size_t>> dims;
+    for (size_t l = 0; l < n_levels; ++l) {
+      need(levels[l] != nullptr, "null level operator");
+      LevelOp o;
+      o.sop = levels[l]->op;
+      dims.emplace_back(o.sop->n1(), o.sop->n2());
+      lv.push_back(o);
+    }
+    auto h = std::make_unique<fde_mg_s>();
+    h->h = std::make_shared<Hierarchy>(std::move(lv), dims, MODE_GEOMETRIC, omega, coarse,
+                                       coarse_sweeps);
+    *out = h.release();
+  });
+}
+
+int fde_mg_build_p2(fde_op fine, double omega, fde_mg* out) {
+  return guard([&] {
+    need(fine && out, "null argument");
+    auto h = std::make_unique<fde_mg_s>();
+    h->h = build_p2_hierarchy(*fine->op, omega);
+    *out = h.release();
+  });
+}
+
+int fde_mg_depth(fde_mg h, size_t* depth) {
+  return guard([&] {
+    need(h && depth, "null argument");
+    *depth = h->h->depth();
+  });
+}
+int fde_mg_level_dims(fde_mg h, size_t level, size_t* n1, size_t* n2) {
+  return guard([&] {
+    need(h && n1 && n2, "null argument");
+    need(level < h->h->depth(), "level out of range");
+    *n1 = h->h->dims(level).first;
+    *n2 = h->h->dims(level).second;
+  });
+}
+int fde_mg_vcycle(fde_mg h, const double* b, double* x, int zero_guess, void* stream) {
+  return guard([&] {
+    need(h && b && x, "null argument");
+    h->h->vcycle(b, x, zero_guess != 0, stream_of(stream));
+  });
+}
+int fde_mg_destroy(fde_mg h) {
+  return guard([&] { delete h; });
+}
+
+int fde_precond_create(int kind, const fde_problem* p, size_t n1, size_t n2, size_t steps,
+                       size_t m, fde_op op, double omega, size_t cycles, int coarse,
+                       size_t coarse_sweeps, fde_precond* out) {
+  return guard([&] {
+    need(out && op, "null argument");
+    auto h = std::make_unique<fde_precond_s>();
+    if (kind == PC_MGM) {
+      const Problem pr = to_problem(p);
+      const Grid g(pr, n1, n2, steps);
+      h->pc = make_pc(kind, pr, g, m, op->op, omega, cycles, coarse, coarse_sweeps);
+    } else {
+      h->pc = make_pc(kind, Problem{}, Grid{}, m, op->op, omega, cycles, coarse, coarse_sweeps);
+    }
+    *out = h.release();
+  });
+}
+int fde_precond_apply(fde_precond pc, const double* r, double* z, void* stream) {
+  return guard([&] {
+    need(pc && r && z, "null argument");
+    pc->pc->apply(r, z, stream_of(stream));
+  });
+}
+int fde_precond_destroy(fde_precond pc) {
+  return guard([&] { delete pc; });
+}
+
+int fde_gmres(fde_op a, fde_precond m, const fde_solver_config* cfg, const double* b,
+              double* x, fde_krylov_result* res, void* stream) {
+  return guard([&] {
+    need(a && cfg && b && x, "null argument");
+    SolverConfig c{cfg->tol, cfg->restart, cfg->max_outer};
+    need(c.restart > 0 && c.tol > 0.0, "invalid solver configuration");
+    KrylovWorkspace& ws = workspace_for(a->ws, a->op->size(), c.restart);
+    fill_result(ws.gmres(*a->op, m ? m->pc.get() : nullptr, c, b, x, stream_of(stream)), res);
+  });
+}
+
+int fde_bicgstab(fde_op a, fde_precond m, const fde_solver_config* cfg, const double* b,
+                 double* x, fde_krylov_result* res, void* stream) {
+  return guard([&] {
+    need(a && cfg && b && x, "null argument");
+    SolverConfig c{cfg->tol, cfg->restart, cfg->max_outer};
+    KrylovWorkspace& ws = workspace_for(a->ws, a->op->size(), c.restart);
+    fill_result(ws.bicgstab(*a->op, m ? m->pc.get() : nullptr, c, b, x, stream_of(stream)),
+                res);
+  });
+}
+
+void fde_driver_config_default(fde_driver_config* c) {
+  if (!c) return;
+  c->precond = PC_NONE;  // driver.hpp:12-21
+  c->tol = 1e-7;
+  c->restart = 20;
+  c->max_outer = 100;
+  c->omega = 0.9;
+  c->cycles = 1;
+  c->coarse = COARSE_SWEEPS;
+  c->coarse_sweeps = 3;
+  c->solver = 0;
+}
+
+int fde_march_create(const fde_problem* p, size_t n1, size_t n2, size_t steps,
+                     const fde_driver_config* cfg, fde_march* out) {
+  return guard([&] {
+    need(out && cfg, "null argument");
+    need(cfg->solver == 0 || cfg->solver == 1, "solver must be 0 (gmres) or 1 (bicgstab)");
+    auto h = std::make_unique<fde_march_s>();
+    h->p = to_problem(p);
+    h->g = Grid(h->p, n1, n2, steps);
+    h->cfg = *cfg;
+    const size_t n = h->g.size();
+    // driver.cpp:22-27: u0, operator and preconditioner (time-independent coefficients)
+    const std::vector<double> u0 = sample_initial(h->p, h->g);
+    h->op = assemble_step_operator(h->p, h->g, 1);
+    h->pc = make_pc(cfg->precond, h->p, h->g, 1, h->op, cfg->omega, cfg->cycles, cfg->coarse,
+                    cfg->coarse_sweeps);
+    h->ws = std::make_unique<KrylovWorkspace>(n, cfg->restart < 5 ? 5 : cfg->restart);
+    h->u.upload(u0.data(), n);
+    h->b.alloc(n);
+    h->src.alloc(n);
+    h->x.alloc(n);
+    h->scale = 2.0 * std::pow(h->g.hx, h->p.alpha);
+    *out = h.release();
+  });
+}
+
+int fde_march_step(fde_march h, const double* source, int source_mode, void* stream,
+                   size_t* iterations, double* residual) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    cudaStream_t s = stream_of(stream);
+    const size_t n = h->g.size();
+    const size_t m = h->m + 1;
+    const double* src = h->src.get();
+    if (source_mode == 0) {
+      if (h->p.preset && h->p.source_kind != 1) {
+        generate_source_device(h->p, h->g, m, h->src.get(), s);  // bit-identical uniforms
+      } else {
+        h->host_src.resize(n);
+        sample_source(h->p, h->g, m, h->host_src.data());
+        FDE_CUDA(cudaMemcpyAsync(h->src.get(), h->host_src.data(), n * sizeof(double),
+                                 cudaMemcpyHostToDevice, s));
+      }
+    } else if (source_mode == 1) {
+      need(source != nullptr, "null source");
+      FDE_CUDA(cudaMemcpyAsync(h->src.get(), source, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    } else if (source_mode == 2) {
+      need(source != nullptr, "null source");
+      src = source;
+    } else {
+      throw InvalidArgument("source_mode must be 0, 1 or 2");
+    }
+    // assemble_rhs (problem.cpp:73-89): b = apply_rhs(u) + 2 hx^alpha v, fused
+    EpiArgs e;
+    e.src = src;
+    e.src_scale = h->scale;
+    h->op->run(h->u.get(), h->b.get(), -1.0, EPI_RHS, e, s);
+    SolverConfig c{h->cfg.tol, h->cfg.restart, h->cfg.max_outer};
+    const Precond* pc = h->pc->kind() == PC_NONE ? nullptr : h->pc.get();
+    const KrylovResult r = h->cfg.solver == 1
+                               ? h->ws->bicgstab(*h->op, pc, c, h->b.get(), h->x.get(), s)
+                               : h->ws->gmres(*h->op, pc, c, h->b.get(), h->x.get(), s);
+    std::swap(h->u, h->x);
+    h->m = m;
+    if (iterations) *iterations = r.total_iterations;
+    if (residual) *residual = r.residual_history.back();
+  });
+}
+
+int fde_march_steps_taken(fde_march h, size_t* m) {
+  return guard([&] {
+    need(h && m, "null argument");
+    *m = h->m;
+  });
+}
+
+int fde_march_solution(fde_march h, double* u, int to_host, void* stream) {
+  return guard([&] {
+    need(h && u, "null argument");
+    cudaStream_t s = stream_of(stream);
+    FDE_CUDA(cudaMemcpyAsync(u, h->u.get(), h->g.size() * sizeof(double),
+                             to_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+    if (to_host) FDE_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int fde_march_solution_ptr(fde_march h, const double** u_dev) {
+  return guard([&] {
+    need(h && u_dev, "null argument");
+    *u_dev = h->u.get();
+  });
+}
+
+int fde_march_destroy(fde_march h) {
+  return guard([&] { delete h; });
+}
+
+int fde_time_march(const fde_problem* p, size_t n1, size_t n2, size_t steps,
+                   const fde_driver_config* cfg, double* solution, size_t* step_iterations,
+                   double* step_residuals, double* wall_seconds) {
+  fde_march h = nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  int rc = fde_march_create(p, n1, n2, steps, cfg, &h);
+  if (rc != FDE_OK) return rc;
+  for (size_t m = 0; m < steps && rc == FDE_OK; ++m) {
+    size_t it = 0;
+    double res = 0.0;
+    rc = fde_march_step(h, nullptr, 0, nullptr, &it, &res);
+    if (step_iterations) step_iterations[m] = it;
+    if (step_residuals) step_residuals[m] = res;
+  }
+  if (rc == FDE_OK && solution) rc = fde_march_solution(h, solution, 1, nullptr);
+  const int rc2 = fde_march_destroy(h);
+  if (wall_seconds)
+    *wall_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return rc != FDE_OK ? rc : rc2;
+}
+
+}  // extern "C"

@@ -1,0 +1,339 @@
+#include <algorithm>
+#include <cmath>
+#include <utility>
+
+#include "krylov.cuh"
+
+namespace fde_b200 {
+namespace {
+
+__global__ void k_copy_scale(size_t n, double a, const double* __restrict__ x,
+                             double* __restrict__ y) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    y[i] = x[i] * a;
+}
+void copy_scale(size_t n, double a, const double* x, double* y, cudaStream_t s) {
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_copy_scale<<<blocks, 256, 0, s>>>(n, a, x, y);
+  FDE_LAUNCH_CHECK();
+}
+
+// p = r + beta (p - omega v)     (BiCGSTAB direction update)
+__global__ void k_bicg_p(size_t n, double beta, double omg, const double* __restrict__ r,
+                         const double* __restrict__ v, double* __restrict__ p) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    p[i] = r[i] + beta * (p[i] - omg * v[i]);
+}
+// s = r - alpha v
+__global__ void k_axpy2(size_t n, double a, const double* __restrict__ x,
+                        const double* __restrict__ y, double* __restrict__ out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    out[i] = y[i] - a * x[i];
+}
+// x += alpha p + omega s
+__global__ void k_bicg_x(size_t n, double alpha, double omg, const double* __restrict__ p,
+                         const double* __restrict__ sv, double* __restrict__ x) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    x[i] += alpha * p[i] + omg * sv[i];
+}
+int nblocks(size_t n) {
+  int b = (int)((n + 255) / 256);
+  return b > 148 * 8 ? 148 * 8 : (b ? b : 1);
+}
+
+// back_substitute (krylov.cpp:19-30)
+std::vector<double> back_substitute(const std::vector<double>& h, size_t ld,
+                                    const std::vector<double>& g, size_t k) {
+  std::vector<double> y(k, 0.0);
+  for (size_t i = k; i-- > 0;) {
+    double v = g[i];
+    for (size_t j = i + 1; j < k; ++j) v -= h[j * ld + i] * y[j];
+    y[i] = h[i * ld + i] != 0.0 ? v / h[i * ld + i] : 0.0;
+  }
+  return y;
+}
+
+}  // namespace
+
+Precond::Precond(int kind, std::shared_ptr<Hierarchy> h, size_t n, size_t cycles)
+    : kind_(kind), h_(std::move(h)), n_(n), cycles_(cycles) {
+  if (kind_ != PC_NONE && !h_) throw InvalidArgument("preconditioner needs a hierarchy");
+  if (kind_ != PC_NONE && cycles_ == 0) throw InvalidArgument("cycles must be >= 1");
+}
+
+void Precond::apply(const double* r, double* z, cudaStream_t s) const {
+  if (kind_ == PC_NONE) {
+    FDE_CUDA(cudaMemcpyAsync(z, r, n_ * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  // z = 0; cycles x vcycle(r, z): the first cycle is the zero-guess path
+  // (the reference scans z, multigrid.cpp:387-392).  With one cycle the
+  // zero fill is dead work: every path of the zero-guess cycle writes z.
+  if (cycles_ > 1 || h_->coarse() == COARSE_NONE)
+    FDE_CUDA(cudaMemsetAsync(z, 0, n_ * sizeof(double), s));
+  for (size_t c = 0; c < cycles_; ++c) h_->vcycle(r, z, c == 0, s);
+}
+
+KrylovWorkspace::KrylovWorkspace(size_t n, size_t restart) : n_(n), rst_(restart) {
+  if (restart == 0) throw InvalidArgument("invalid solver configuration");
+  v_.resize(rst_ + 1);
+  std::vector<const double*> ptrs(rst_ + 1);
+  for (size_t k = 0; k <= rst_; ++k) {
+    v_[k].alloc(n);
+    ptrs[k] = v_[k].get();
+  }
+  for (DevBuf<double>* b : {&t_, &r_, &z_, &w_, &trial_}) b->alloc(n);
+  dsc_.alloc(4 * (rst_ + 2) + 16);
+  dcoef_.alloc(rst_ + 1);
+  dptr_.upload(ptrs.data(), ptrs.size());
+  FDE_CUDA(cudaMallocHost(&hsc_, sizeof(double) * (4 * (rst_ + 2) + 16 + rst_ + 1)));
+}
+
+void KrylovWorkspace::precondition(const Precond* m, const double* r, double* z,
+                                   cudaStream_t s) {
+  if (m) m->apply(r, z, s);
+  else FDE_CUDA(cudaMemcpyAsync(z, r, n_ * sizeof(double), cudaMemcpyDeviceToDevice, s));
+}
+
+void KrylovWorkspace::fetch(size_t count, cudaStream_t s) {
+  FDE_CUDA(cudaMemcpyAsync(hsc_, dsc_.get(), count * sizeof(double), cudaMemcpyDeviceToHost, s));
+  FDE_CUDA(cudaStreamSynchronize(s));
+}
+
+double KrylovWorkspace::nrm2_host(const double* v, cudaStream_t s) {
+  red_.dot(n_, v, v, dsc_.get(), s, true);
+  fetch(1, s);
+  return hsc_[0];
+}
+
+double KrylovWorkspace::dot_host(const double* x, const double* y, cudaStream_t s) {
+  red_.dot(n_, x, y, dsc_.get(), s, false);
+  fetch(1, s);
+  return hsc_[0];
+}
+
+double KrylovWorkspace::true_rel(const StructuredOp& a, const Precond* m, const double* b,
+                                 const double* x, double norm_b, cudaStream_t s) {
+  EpiArgs e;
+  e.b = b;
+  a.run(x, r_.get(), 1.0, EPI_RESID, e, s);  // r = b - A x (krylov.cpp:60-61)
+  precondition(m, r_.get(), z_.get(), s);
+  return nrm2_host(z_.get(), s) / norm_b;
+}
+
+KrylovResult KrylovWorkspace::gmres(const StructuredOp& a, const Precond* m,
+                                    const SolverConfig& cfg, const double* b, double* x_out,
+                                    cudaStream_t s) {
+  const size_t n = n_;
+  if (a.size() != n) throw InvalidArgument("rhs size mismatch");
+  if (cfg.restart == 0 || !(cfg.tol > 0.0)) throw InvalidArgument("invalid solver configuration");
+  if (cfg.restart > rst_) throw InvalidArgument("restart exceeds the workspace");
+  const size_t rst = cfg.restart, ld = rst + 1;
+  KrylovResult res;
+  double* x = x_out;
+  double* trial = trial_.get();
+  FDE_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+
+  precondition(m, b, z_.get(), s);
+  const double norm_b = nrm2_host(z_.get(), s);
+  if (norm_b == 0.0) {
+    res.converged = true;
+    res.residual_history.push_back(0.0);
+    return res;
+  }
+  std::vector<double> h(ld * rst, 0.0), g(ld, 0.0), cs(rst, 0.0), sn(rst, 0.0), y;
+  double* const dh = dsc_.get();              // h column slots [0, rst]
+  double* const dnorm0 = dsc_.get() + ld;     // ||w|| before MGS
+  double* const dnrmw = dsc_.get() + ld + 1;  // ||w|| after MGS
+  double* const dreo = dsc_.get() + ld + 2;   // re-orthogonalisation coefficients
+  auto lincomb_into = [&](const double* x0, double* out, const std::vector<double>& coef) {
+    std::copy(coef.begin(), coef.end(), hsc_ + 4 * (rst_ + 2) + 16);
+    FDE_CUDA(cudaMemcpyAsync(dcoef_.get(), hsc_ + 4 * (rst_ + 2) + 16,
+                             coef.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    vec_lincomb(n, x0, dptr_.get(), dcoef_.get(), (int)coef.size(), out, s);
+    FDE_CUDA(cudaStreamSynchronize(s));  // the pinned staging slot is reused
+  };
+
+  for (size_t outer = 0; outer < cfg.max_outer && !res.converged; ++outer) {
+    EpiArgs e;
+    e.b = b;
+    a.run(x, r_.get(), 1.0, EPI_RESID, e, s);  // r = b - A x
+    precondition(m, r_.get(), z_.get(), s);
+    const double beta = nrm2_host(z_.get(), s);
+    const double rel0 = beta / norm_b;
+    if (outer == 0) res.residual_history.push_back(rel0);
+    if (rel0 <= cfg.tol) {
+      res.converged = true;
+      break;
+    }
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    copy_scale(n, 1.0 / beta, z_.get(), v_[0].get(), s);  // scal(1/beta); v[0] = z
+
+    size_t spanned = 0;
+    bool cycle_done = false;
+    for (size_t i = 0; i < rst && !cycle_done; ++i) {
+      a.apply(v_[i].get(), t_.get(), s);
+      precondition(m, t_.get(), w_.get(), s);
+      red_.dot(n, w_.get(), w_.get(), dnorm0, s, true);
+      for (size_t k = 0; k <= i; ++k) {  // modified Gram-Schmidt
+        red_.dot(n, v_[k].get(), w_.get(), dh + k, s);
+        vec_axpy_dev(n, dh + k, -1.0, v_[k].get(), w_.get(), s);
+      }
+      red_.dot(n, w_.get(), w_.get(), dnrmw, s, true);
+      fetch(ld + 2, s);
+      for (size_t k = 0; k <= i; ++k) h[i * ld + k] = hsc_[k];
+      const double norm0 = hsc_[ld];
+      double hip = hsc_[ld + 1];
+      if (hip < 1e-8 * norm0) {  // second pass (krylov.cpp:98-104)
+        for (size_t k = 0; k <= i; ++k) {
+          red_.dot(n, v_[k].get(), w_.get(), dreo + k, s);
+          vec_axpy_dev(n, dreo + k, -1.0, v_[k].get(), w_.get(), s);
+        }
+        red_.dot(n, w_.get(), w_.get(), dnrmw, s, true);
+        fetch(ld + 2 + i + 1, s);
+        for (size_t k = 0; k <= i; ++k) h[i * ld + k] += hsc_[ld + 2 + k];
+        hip = hsc_[ld + 1];
+      }
+      const bool happy = hip <= 1e-14 * (norm0 > 0.0 ? norm0 : 1.0);
+
+      for (size_t k = 0; k + 1 <= i; ++k) {  // apply previous rotations
+        const double tmp = cs[k] * h[i * ld + k] + sn[k] * h[i * ld + k + 1];
+        h[i * ld + k + 1] = -sn[k] * h[i * ld + k] + cs[k] * h[i * ld + k + 1];
+        h[i * ld + k] = tmp;
+      }
+      const double denom = std::hypot(h[i * ld + i], hip);
+      cs[i] = denom > 0.0 ? h[i * ld + i] / denom : 1.0;
+      sn[i] = denom > 0.0 ? hip / denom : 0.0;
+      h[i * ld + i] = denom;
+      g[i + 1] = -sn[i] * g[i];
+      g[i] = cs[i] * g[i];
+
+      ++res.total_iterations;
+      spanned = i + 1;
+      const double est = std::fabs(g[i + 1]) / norm_b;
+      res.residual_history.push_back(est);
+      if (!happy) copy_scale(n, 1.0 / hip, w_.get(), v_[i + 1].get(), s);
+
+      if (est <= cfg.tol || happy) {  // verify the estimate (krylov.cpp:132-149)
+        y = back_substitute(h, ld, g, spanned);
+        lincomb_into(x, trial, y);
+        std::swap(x, trial);
+        if (true_rel(a, m, b, x, norm_b, s) <= cfg.tol) {
+          res.converged = true;
+          cycle_done = true;
+        } else if (happy) {
+          cycle_done = true;
+        } else {
+          std::swap(x, trial);  // estimate lied: keep iterating
+        }
+      }
+    }
+    if (!res.converged && !cycle_done) {
+      y = back_substitute(h, ld, g, spanned);
+      lincomb_into(x, x, y);
+    }
+  }
+  const double final_rel = true_rel(a, m, b, x, norm_b, s);
+  if (final_rel <= cfg.tol) res.converged = true;
+  if (res.residual_history.empty()) res.residual_history.push_back(final_rel);
+  else res.residual_history.back() = final_rel;
+  if (x != x_out)
+    FDE_CUDA(cudaMemcpyAsync(x_out, x, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  return res;
+}
+
+KrylovResult KrylovWorkspace::bicgstab(const StructuredOp& a, const Precond* m,
+                                       const SolverConfig& cfg, const double* b, double* x,
+                                       cudaStream_t s) {
+  const size_t n = n_;
+  if (a.size() != n) throw InvalidArgument("rhs size mismatch");
+  if (cfg.restart == 0 || cfg.max_outer == 0 || !(cfg.tol > 0.0))
+    throw InvalidArgument("invalid solver configuration");
+  // BiCGSTAB vectors reuse the Arnoldi basis storage
+  if (rst_ < 5) throw InvalidArgument("bicgstab needs a workspace with restart >= 5");
+  double *r = v_[0].get(), *rh = v_[1].get(), *p = v_[2].get(), *v = v_[3].get(),
+         *sv = v_[4].get(), *tv = v_[5 % (rst_ + 1)].get();
+  double *tmp = t_.get(), *tmp2 = r_.get();
+  const size_t max_it = cfg.restart * cfg.max_outer;
+  KrylovResult res;
+  FDE_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+  precondition(m, b, r, s);  // r = M^-1 (b - A 0)
+  const double norm_b = nrm2_host(r, s);
+  if (norm_b == 0.0) {
+    res.converged = true;
+    res.residual_history.push_back(0.0);
+    return res;
+  }
+  FDE_CUDA(cudaMemcpyAsync(rh, r, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  res.residual_history.push_back(1.0);
+  auto true_res = [&](const double* xv, double* out) {  // out = M^-1 (b - A xv)
+    EpiArgs e;
+    e.b = b;
+    a.run(xv, tmp2, 1.0, EPI_RESID, e, s);
+    precondition(m, tmp2, out, s);
+    return nrm2_host(out, s) / norm_b;
+  };
+  double rho = 1.0, alpha = 1.0, omg = 1.0;
+  for (size_t it = 0; it < max_it; ++it) {
+    const double rho_new = dot_host(rh, r, s);
+    if (rho_new == 0.0) break;
+    if (it == 0) {
+      FDE_CUDA(cudaMemcpyAsync(p, r, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    } else {
+      const double beta = (rho_new / rho) * (alpha / omg);
+      k_bicg_p<<<nblocks(n), 256, 0, s>>>(n, beta, omg, r, v, p);
+      FDE_LAUNCH_CHECK();
+    }
+    a.apply(p, tmp, s);
+    precondition(m, tmp, v, s);
+    const double rv = dot_host(rh, v, s);
+    if (rv == 0.0) break;
+    alpha = rho_new / rv;
+    k_axpy2<<<nblocks(n), 256, 0, s>>>(n, alpha, v, r, sv);  // s = r - alpha v
+    FDE_LAUNCH_CHECK();
+    ++res.total_iterations;
+    const double srel = nrm2_host(sv, s) / norm_b;
+    if (srel <= cfg.tol) {  // half step: verify x + alpha p
+      double* trial = trial_.get();
+      FDE_CUDA(cudaMemcpyAsync(trial, x, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      vec_axpy(n, alpha, p, trial, s);
+      const double trel = true_res(trial, tv);
+      if (trel <= cfg.tol) {
+        FDE_CUDA(cudaMemcpyAsync(x, trial, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        res.residual_history.push_back(trel);
+        res.converged = true;
+        break;
+      }
+    }
+    a.apply(sv, tmp, s);
+    precondition(m, tmp, tv, s);
+    const double tt = dot_host(tv, tv, s);
+    omg = tt > 0.0 ? dot_host(tv, sv, s) / tt : 0.0;
+    k_bicg_x<<<nblocks(n), 256, 0, s>>>(n, alpha, omg, p, sv, x);
+    FDE_LAUNCH_CHECK();
+    k_axpy2<<<nblocks(n), 256, 0, s>>>(n, omg, tv, sv, r);  // r = s - omega t
+    FDE_LAUNCH_CHECK();
+    rho = rho_new;
+    const double rel = nrm2_host(r, s) / norm_b;
+    res.residual_history.push_back(rel);
+    if (rel <= cfg.tol) {
+      if (true_res(x, tmp) <= cfg.tol) {
+        res.converged = true;
+        break;
+      }
+    }
+    if (omg == 0.0) break;
+  }
+  const double final_rel = true_res(x, tmp);
+  if (final_rel <= cfg.tol) res.converged = true;
+  res.residual_history.back() = final_rel;
+  return res;
+}
+
+}  // namespace fde_b200

@@ -1,0 +1,111 @@
+// Batched Toeplitz line convolutions for the CN-WSGD operator apply.
+//
+// Restates StructuredFdeOperator::apply_impl (proj/src/structured.cpp:125-148)
+// and ToeplitzBlock::apply_both (structured.cpp:74-89) the B200 way:
+//
+//  * Every grid line is one independent job: T x and T^T x of a lower
+//    Hessenberg Toeplitz block via its length-L = next_pow2(2n-1) circulant
+//    embedding.  The reference does 3 complex length-L FFTs per line; here a
+//    real line costs 3 complex FFTs of length M = L/2 (real-input packing
+//    z_m = x_2m + i x_2m+1 on the way in, the two real outputs T x and T^T x
+//    unpacked the same way on the way out), and spectrum(T^T) = conj
+//    spectrum(T) (c is real) so only one spectrum is stored, pre-scaled by
+//    1/(2L) so the whole pipeline runs unnormalised transforms.
+//  * FFTs are Stockham radix-8 (+ one radix-4/2 stage) with 8 points per
+//    thread held in registers; shared memory is only the exchange buffer
+//    between stages (SoA re/im, padded every 32 doubles against bank
+//    conflicts).  Twiddles are plain (non-__ldg) loads so ptxas cannot hoist
+//    them across the stage barriers (that blew the register budget).
+//  * Two passes per apply: the y-pass (columns, stride n1) runs first and
+//    writes Q = sign * s/r * (ep T_b x + em T_b^T x) using pre-transposed
+//    ep/em; the x-pass (rows, contiguous) adds inv_r x + sign (dp T_a x +
+//    dm T_a^T x) + Q and applies a fused epilogue (plain store, rhs source
+//    add, residual b - Ax, damped-Jacobi update) -- all its streams coalesced.
+//  * Lines with n <= kDirectMax use a warp-per-line direct product (coarse
+//    multigrid levels, semicoarsened n = 1 lines).
+#pragma once
+#include "common.cuh"
+
+namespace fde_b200 {
+
+constexpr int kDirectMax = 32;  // n <= this: direct Toeplitz product
+
+// One Toeplitz block resident in HBM (built by ToeplitzDev, operator.cu).
+struct LineBlockDev {
+  int n;                 // line length
+  int logM;              // FFT path: M = 2^logM = L/2; 0 -> direct path
+  const double2* spec;   // S[k] / (2L), k = 0..M  (S = DFT_L of the circulant column)
+  const double2* twM;    // exp(-2 pi i k / M), k < M
+  const double2* twL;    // exp(-2 pi i k / L), k < M
+  const double* col;     // first column, n entries (direct path)
+  const double* row;     // first row, n entries (direct path)
+};
+
+enum Epilogue : int {
+  EPI_STORE = 0,   // out = A x                       (LinOp::apply)
+  EPI_RHS = 1,     // out = A~ x + src_scale * src     (assemble_rhs, problem.cpp:73-89)
+  EPI_RESID = 2,   // out = b - A x                    (multigrid.cpp:363-364, krylov.cpp:71-72)
+  EPI_JACOBI = 3,  // out = x + omega dinv (b - A x)   (multigrid.cpp:380-382)
+};
+
+// Column pass: line = x index i, position = y index j (stride n1).
+struct YPass {
+  static constexpr bool kNeedsX = false;
+  LineBlockDev blk;
+  int n1, n2;
+  const double* x;
+  const double* epT;  // ep transposed: epT[i * n2 + j] = ep[i + j * n1]
+  const double* emT;
+  double c;           // sign * s_over_r
+  double* q;          // Q[i + j * n1]
+  __device__ __forceinline__ int nlines() const { return n1; }
+  __device__ __forceinline__ double load(int line, int pos) const {
+    return x[(size_t)pos * n1 + line];
+  }
+  __device__ __forceinline__ void store(int line, int pos, double ty, double tt, double) const {
+    const size_t t = (size_t)line * n2 + pos;
+    q[(size_t)pos * n1 + line] = c * (epT[t] * ty + emT[t] * tt);
+  }
+};
+
+// Row pass: line = y index j, position = x index i (contiguous).
+struct XPass {
+  static constexpr bool kNeedsX = true;
+  LineBlockDev blk;
+  int n1, n2;
+  const double* x;
+  const double* dp;
+  const double* dm;
+  const double* q;     // y-pass result (nullptr: no y term)
+  double inv_r, sign;
+  int epi;
+  double* out;
+  const double* b;     // EPI_RESID / EPI_JACOBI
+  const double* dinv;  // EPI_JACOBI
+  double omega;
+  const double* src;   // EPI_RHS
+  double src_scale;
+  __device__ __forceinline__ int nlines() const { return n2; }
+  __device__ __forceinline__ double load(int line, int pos) const {
+    return x[(size_t)line * n1 + pos];
+  }
+  __device__ __forceinline__ void store(int line, int pos, double ty, double tt, double xv) const {
+    const size_t p = (size_t)line * n1 + pos;
+    // structured.cpp:128,134-135,146: y = inv_r x; y += s dp t; y += s dm tt; y += Q
+    double y = inv_r * xv;
+    y += sign * dp[p] * ty;
+    y += sign * dm[p] * tt;
+    if (q) y += q[p];
+    switch (epi) {
+      case EPI_RHS: out[p] = y + src_scale * src[p]; break;
+      case EPI_RESID: out[p] = b[p] - y; break;
+      case EPI_JACOBI: out[p] = xv + omega * dinv[p] * (b[p] - y); break;
+      default: out[p] = y; break;
+    }
+  }
+};
+
+void launch_line_pass(const YPass& p, cudaStream_t s);
+void launch_line_pass(const XPass& p, cudaStream_t s);
+
+}  // namespace fde_b200

@@ -1,0 +1,247 @@
+// Host setup of the device-resident operator: WSGD weights, circulant
+// spectra, twiddle tables, coefficient fields (reference structured.cpp,
+// weights.cpp).  Setup arithmetic runs once per level in long double so the
+// device tables are correctly rounded.
+#include <cmath>
+#include <complex>
+#include <map>
+#include <mutex>
+
+#include "operator.cuh"
+
+namespace fde_b200 {
+
+std::vector<double> binom_coeffs(double gamma, size_t K) {
+  if (!(gamma > 1.0) || !(gamma <= 2.0))
+    throw InvalidArgument("weights: gamma must lie in (1, 2]");
+  std::vector<double> g(K + 1);
+  g[0] = 1.0;
+  for (size_t k = 1; k <= K; ++k) g[k] = g[k - 1] * (1.0 - (gamma + 1.0) / double(k));
+  return g;
+}
+
+std::vector<double> wsgd_weights(double gamma, size_t K, int pq) {
+  if (K < 2) throw InvalidArgument("weights: K must be >= 2");
+  const std::vector<double> g = binom_coeffs(gamma, K);
+  std::vector<double> w(K + 1);
+  if (pq == 0) {
+    const double cg = 0.5 * gamma, cg1 = 0.5 * (2.0 - gamma);
+    w[0] = cg;
+    for (size_t k = 1; k <= K; ++k) w[k] = cg * g[k] + cg1 * g[k - 1];
+  } else if (pq == 1) {
+    const double l1 = (gamma + 2.0) / 4.0, l2 = (2.0 - gamma) / 4.0;
+    for (size_t k = 0; k <= K; ++k) w[k] = l1 * g[k] + (k >= 2 ? l2 * g[k - 2] : 0.0);
+  } else {
+    throw InvalidArgument("weights: (p,q) selector must be 0 for (1,0) or 1 for (1,-1)");
+  }
+  return w;
+}
+
+size_t next_pow2(size_t n) {
+  size_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+namespace {
+
+using cld = std::complex<long double>;
+constexpr long double kPiL = 3.141592653589793238462643383279502884L;
+
+// exp(-2 pi i k / n), correctly rounded to double via long double.
+double2 unit_root(size_t k, size_t n) {
+  const long double a = 2.0L * kPiL * (long double)k / (long double)n;
+  return make_double2((double)cosl(a), (double)-sinl(a));
+}
+
+// In-place forward DFT of power-of-two length in long double (setup only).
+void fft_ld(std::vector<cld>& a) {
+  const size_t n = a.size();
+  if (n <= 1) return;
+  for (size_t i = 1, j = 0; i < n; ++i) {
+    size_t bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) std::swap(a[i], a[j]);
+  }
+  for (size_t len = 2; len <= n; len <<= 1) {
+    for (size_t k = 0; k < len / 2; ++k) {
+      const long double ang = -2.0L * kPiL * (long double)k / (long double)len;
+      const cld w(cosl(ang), sinl(ang));
+      for (size_t i = 0; i < n; i += len) {
+        const cld u = a[i + k], v = a[i + k + len / 2] * w;
+        a[i + k] = u + v;
+        a[i + k + len / 2] = u - v;
+      }
+    }
+  }
+}
+
+struct TwiddleTables {
+  DevBuf<double2> twM, twL;
+};
+
+const TwiddleTables& twiddles(int logM) {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<TwiddleTables>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& slot = cache[logM];
+  if (!slot) {
+    const size_t M = size_t(1) << logM;
+    std::vector<double2> tm(M), tl(M);
+    for (size_t k = 0; k < M; ++k) {
+      tm[k] = unit_root(k, M);
+      tl[k] = unit_root(k, 2 * M);
+    }
+    auto t = std::make_unique<TwiddleTables>();
+    t->twM.upload(tm.data(), M);
+    t->twL.upload(tl.data(), M);
+    slot = std::move(t);
+  }
+  return *slot;
+}
+
+}  // namespace
+
+ToeplitzDev::ToeplitzDev(std::vector<double> first_col, std::vector<double> first_row)
+    : n_(first_col.size()), col_(std::move(first_col)), row_(std::move(first_row)) {
+  if (n_ == 0 || row_.size() != n_)
+    throw InvalidArgument("toeplitz column and row sizes must match");
+  if (col_[0] != row_[0]) throw InvalidArgument("toeplitz corner entry mismatch");
+  L_ = next_pow2(2 * n_ - 1);
+  dcol_ = std::make_shared<DevBuf<double>>();
+  drow_ = std::make_shared<DevBuf<double>>();
+  dcol_->upload(col_.data(), n_);
+  drow_->upload(row_.data(), n_);
+  if (n_ <= size_t(kDirectMax)) {
+    logM_ = 0;
+    return;
+  }
+  const size_t M = L_ / 2;
+  logM_ = 0;
+  while ((size_t(1) << logM_) < M) ++logM_;
+  if (logM_ > 12) throw InvalidArgument("line length beyond the supported FFT sizes (n <= 4095)");
+  // circulant column (structured.cpp:21-30), spectrum scaled by 1/(2L)
+  std::vector<cld> c(L_, cld(0.0L, 0.0L));
+  for (size_t i = 0; i < n_; ++i) c[i] = (long double)col_[i];
+  for (size_t j = 1; j < n_; ++j) c[L_ - j] = (long double)row_[j];
+  fft_ld(c);
+  std::vector<double2> s(M + 1);
+  const long double sc = 1.0L / (2.0L * (long double)L_);
+  for (size_t k = 0; k <= M; ++k)
+    s[k] = make_double2((double)(c[k].real() * sc), (double)(c[k].imag() * sc));
+  spec_ = std::make_shared<DevBuf<double2>>();
+  spec_->upload(s.data(), s.size());
+}
+
+ToeplitzDev ToeplitzDev::fractional(double gamma, size_t n, int pq) {
+  if (n == 0) throw InvalidArgument("empty toeplitz block");
+  const std::vector<double> w = wsgd_weights(gamma, n < 2 ? 2 : n, pq);
+  std::vector<double> col(n), row(n, 0.0);
+  for (size_t i = 0; i < n; ++i) col[i] = -w[i + 1];
+  row[0] = -w[1];
+  if (n > 1) row[1] = -w[0];
+  return ToeplitzDev(std::move(col), std::move(row));
+}
+
+LineBlockDev ToeplitzDev::dev() const {
+  LineBlockDev d{};
+  d.n = (int)n_;
+  d.logM = logM_;
+  d.col = dcol_->get();
+  d.row = drow_->get();
+  if (logM_) {
+    const TwiddleTables& t = twiddles(logM_);
+    d.spec = spec_->get();
+    d.twM = t.twM.get();
+    d.twL = t.twL.get();
+  }
+  return d;
+}
+
+StructuredOp::StructuredOp(size_t n1, size_t n2, double inv_r, double s_over_r,
+                           ToeplitzDev ax, ToeplitzDev ay, std::vector<double> dp,
+                           std::vector<double> dm, std::vector<double> ep,
+                           std::vector<double> em)
+    : n1_(n1), n2_(n2), inv_r_(inv_r), s_over_r_(s_over_r), ax_(std::move(ax)),
+      ay_(std::move(ay)), dp_(std::move(dp)), dm_(std::move(dm)), ep_(std::move(ep)),
+      em_(std::move(em)) {
+  const size_t n = n1_ * n2_;
+  if (n == 0) throw InvalidArgument("empty operator");
+  if (ax_.size() != n1_ || ay_.size() != n2_)
+    throw InvalidArgument("toeplitz block size mismatch");
+  if (dp_.size() != n || dm_.size() != n || ep_.size() != n || em_.size() != n)
+    throw InvalidArgument("coefficient field size mismatch");
+  if (!(inv_r_ > 0.0)) throw InvalidArgument("1/r must be positive");
+  if (!(s_over_r_ > 0.0)) throw InvalidArgument("s/r must be positive");
+  for (size_t p = 0; p < n; ++p)
+    if (dp_[p] < 0.0 || dm_[p] < 0.0 || ep_[p] < 0.0 || em_[p] < 0.0)
+      throw InvalidArgument("negative diffusion coefficient sample");
+  const double ax0 = ax_.first_col()[0];
+  const double ay0 = ay_.first_col()[0];
+  diag_.resize(n);
+  for (size_t p = 0; p < n; ++p)
+    diag_[p] = inv_r_ + (dp_[p] + dm_[p]) * ax0 + s_over_r_ * (ep_[p] + em_[p]) * ay0;
+  upload();
+  d_q_.alloc(n);
+}
+
+void StructuredOp::upload() {
+  const size_t n = n1_ * n2_;
+  d_dp_.upload(dp_.data(), n);
+  d_dm_.upload(dm_.data(), n);
+  d_diag_.upload(diag_.data(), n);
+  std::vector<double> t(n);  // ep/em transposed for the column pass
+  for (size_t j = 0; j < n2_; ++j)
+    for (size_t i = 0; i < n1_; ++i) t[i * n2_ + j] = ep_[i + j * n1_];
+  d_epT_.upload(t.data(), n);
+  for (size_t j = 0; j < n2_; ++j)
+    for (size_t i = 0; i < n1_; ++i) t[i * n2_ + j] = em_[i + j * n1_];
+  d_emT_.upload(t.data(), n);
+}
+
+void StructuredOp::scale(double s) {
+  inv_r_ *= s;
+  s_over_r_ *= s;
+  for (double& v : dp_) v *= s;
+  for (double& v : dm_) v *= s;
+  for (double& v : diag_) v *= s;
+  const size_t n = n1_ * n2_;
+  d_dp_.upload(dp_.data(), n);
+  d_dm_.upload(dm_.data(), n);
+  d_diag_.upload(diag_.data(), n);
+}
+
+void StructuredOp::run(const double* x, double* out, double sign, int epi, const EpiArgs& e,
+                       cudaStream_t s) const {
+  YPass yp{};
+  yp.blk = ay_.dev();
+  yp.n1 = (int)n1_;
+  yp.n2 = (int)n2_;
+  yp.x = x;
+  yp.epT = d_epT_.get();
+  yp.emT = d_emT_.get();
+  yp.c = sign * s_over_r_;
+  yp.q = d_q_.get();
+  launch_line_pass(yp, s);
+  XPass xp{};
+  xp.blk = ax_.dev();
+  xp.n1 = (int)n1_;
+  xp.n2 = (int)n2_;
+  xp.x = x;
+  xp.dp = d_dp_.get();
+  xp.dm = d_dm_.get();
+  xp.q = d_q_.get();
+  xp.inv_r = inv_r_;
+  xp.sign = sign;
+  xp.epi = epi;
+  xp.out = out;
+  xp.b = e.b;
+  xp.dinv = e.dinv;
+  xp.omega = e.omega;
+  xp.src = e.src;
+  xp.src_scale = e.src_scale;
+  launch_line_pass(xp, s);
+}
+
+}  // namespace fde_b200

@@ -1,0 +1,278 @@
+#include "vec_kernels.cuh"
+
+namespace fde_b200 {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxBlocks = 148 * 8;
+
+inline int blocks_for(size_t n) {
+  const size_t b = (n + kThreads - 1) / kThreads;
+  return (int)(b < (size_t)kMaxBlocks ? (b ? b : 1) : kMaxBlocks);
+}
+
+#define GRID_STRIDE(i, n) \
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (n); i += (size_t)gridDim.x * blockDim.x)
+
+__global__ void k_diag_scale(size_t n, double a, const double* __restrict__ d,
+                             const double* __restrict__ b, double* __restrict__ x) {
+  GRID_STRIDE(i, n) x[i] = a * d[i] * b[i];
+}
+__global__ void k_axpy(size_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  GRID_STRIDE(i, n) y[i] = fma(a, x[i], y[i]);
+}
+__global__ void k_axpy_dev(size_t n, const double* __restrict__ a, double sgn,
+                           const double* __restrict__ x, double* __restrict__ y) {
+  const double av = sgn * *a;
+  GRID_STRIDE(i, n) y[i] = fma(av, x[i], y[i]);
+}
+__global__ void k_scale_inv_dev(size_t n, const double* __restrict__ a, const double* x,
+                                double* y) {
+  const double inv = 1.0 / *a;
+  GRID_STRIDE(i, n) y[i] = x[i] * inv;
+}
+__global__ void k_scal(size_t n, double a, double* x) {
+  GRID_STRIDE(i, n) x[i] *= a;
+}
+__global__ void k_sub(size_t n, const double* __restrict__ x, const double* __restrict__ y,
+                      double* out) {
+  GRID_STRIDE(i, n) out[i] = x[i] - y[i];
+}
+__global__ void k_lincomb(size_t n, const double* x0, const double* const* __restrict__ v,
+                          const double* __restrict__ c, int k, double* out) {
+  GRID_STRIDE(i, n) {
+    double acc = x0[i];
+    for (int q = 0; q < k; ++q) acc = fma(c[q], v[q][i], acc);
+    out[i] = acc;
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void k_dot(size_t n, const double* __restrict__ x, const double* __restrict__ y,
+                      double* __restrict__ partials, unsigned int* counter, double* out,
+                      int sqrt_out) {
+  __shared__ double ws[kThreads / 32];
+  __shared__ bool last;
+  double acc = 0.0;
+  GRID_STRIDE(i, n) acc = fma(x[i], y[i], acc);
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < kThreads / 32 ? ws[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) {
+      partials[blockIdx.x] = v;
+      __threadfence();
+      last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  if (!last) return;
+  // last block: fixed-order sum of the partials (deterministic)
+  __threadfence();
+  double v = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) v += ((volatile double*)partials)[b];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) t += ws[w];
+    *out = sqrt_out ? sqrt(t) : t;
+    *counter = 0u;
+  }
+}
+
+// ---- grid transfers ---------------------------------------------------------
+// restrict_rows (multigrid.cpp:46-58): v = f[fc]; v += .5 f[fc-1]; v += .5 f[fc+1]; scale*v
+__device__ __forceinline__ double rrow(const double* f, int n, int fc, double sc) {
+  double v = f[fc];
+  if (fc > 0) v += 0.5 * f[fc - 1];
+  if (fc + 1 < n) v += 0.5 * f[fc + 1];
+  return sc * v;
+}
+
+__global__ void k_restrict(Xfer t, const double* __restrict__ f, double* __restrict__ c,
+                           double sc) {
+  const size_t nc = (size_t)t.k1 * t.k2;
+  GRID_STRIDE(q, nc) {
+    const int a = (int)(q % t.k1), bb = (int)(q / t.k1);
+    double out;
+    if (!t.cx) {  // restrict_cols only (multigrid.cpp:60-71)
+      const int fb = 2 * bb + 1 - t.par2;
+      double v = f[(size_t)fb * t.n1 + a];
+      if (fb > 0) v += 0.5 * f[(size_t)(fb - 1) * t.n1 + a];
+      if (fb + 1 < t.n2) v += 0.5 * f[(size_t)(fb + 1) * t.n1 + a];
+      out = v * sc;
+    } else if (!t.cy) {  // restrict_rows only
+      out = rrow(f + (size_t)bb * t.n1, t.n1, 2 * a + 1 - t.par1, sc);
+    } else {  // rows then columns of the row-restricted temporary
+      const int fa = 2 * a + 1 - t.par1, fb = 2 * bb + 1 - t.par2;
+      double v = rrow(f + (size_t)fb * t.n1, t.n1, fa, sc);
+      if (fb > 0) v += 0.5 * rrow(f + (size_t)(fb - 1) * t.n1, t.n1, fa, sc);
+      if (fb + 1 < t.n2) v += 0.5 * rrow(f + (size_t)(fb + 1) * t.n1, t.n1, fa, sc);
+      out = v * sc;
+    }
+    c[q] = out;
+  }
+}
+
+// 1D prolongation weight accumulation in the reference order: fine index i
+// receives 1.0 * c[j] if i is a coarse point, else 0.5*c[left] then 0.5*c[right].
+__device__ __forceinline__ double prow(const double* c, int k, int i, int par) {
+  // coarse j sits at fine 2j+1-par
+  const int t = i - 1 + par;  // = 2j when i is the coarse point of j
+  if ((t & 1) == 0) {
+    const int j = t >> 1;
+    return (j >= 0 && j < k) ? c[j] : 0.0;  // 0 + 1.0*c
+  }
+  const int jl = (t - 1) >> 1, jr = jl + 1;  // fine i = fc(jl)+1 = fc(jr)-1
+  double v = 0.0;
+  if (jl >= 0 && jl < k) v += 0.5 * c[jl];
+  if (jr >= 0 && jr < k) v += 0.5 * c[jr];
+  return v;
+}
+
+template <bool ADD>
+__global__ void k_prolong(Xfer t, const double* __restrict__ c, double* __restrict__ f) {
+  const size_t nf = (size_t)t.n1 * t.n2;
+  GRID_STRIDE(q, nf) {
+    const int i = (int)(q % t.n1), j = (int)(q / t.n1);
+    double v;
+    if (!t.cx) {  // prolong_cols only: rows of width n1 (multigrid.cpp:34-44)
+      const int tt = j - 1 + t.par2;
+      if ((tt & 1) == 0) {
+        const int jc = tt >> 1;
+        v = (jc >= 0 && jc < t.k2) ? c[(size_t)jc * t.n1 + i] : 0.0;
+      } else {
+        const int jl = (tt - 1) >> 1, jr = jl + 1;
+        v = 0.0;
+        if (jl >= 0 && jl < t.k2) v += 0.5 * c[(size_t)jl * t.n1 + i];
+        if (jr >= 0 && jr < t.k2) v += 0.5 * c[(size_t)jr * t.n1 + i];
+      }
+    } else if (!t.cy) {  // prolong_rows only
+      v = prow(c + (size_t)j * t.k1, t.k1, i, t.par1);
+    } else {  // rows into tmp (n1 x k2), then columns
+      const int tt = j - 1 + t.par2;
+      if ((tt & 1) == 0) {
+        const int jc = tt >> 1;
+        v = (jc >= 0 && jc < t.k2) ? prow(c + (size_t)jc * t.k1, t.k1, i, t.par1) : 0.0;
+      } else {
+        const int jl = (tt - 1) >> 1, jr = jl + 1;
+        v = 0.0;
+        if (jl >= 0 && jl < t.k2) v += 0.5 * prow(c + (size_t)jl * t.k1, t.k1, i, t.par1);
+        if (jr >= 0 && jr < t.k2) v += 0.5 * prow(c + (size_t)jr * t.k1, t.k1, i, t.par1);
+      }
+    }
+    if (ADD) f[q] += v;
+    else f[q] = v;
+  }
+}
+
+// Single-CTA forward/back substitution with a row-pivoted LU (column-major).
+__global__ void k_lu_solve(int n, const double* __restrict__ lu, const int* __restrict__ perm,
+                           const double* __restrict__ b, double* __restrict__ x) {
+  extern __shared__ double y[];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = b[perm[i]];
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {  // L (unit diagonal): y_i -= l_ij y_j
+    const double yj = y[j];
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) y[i] -= lu[i + (size_t)j * n] * yj;
+    __syncthreads();
+  }
+  for (int j = n - 1; j >= 0; --j) {  // U
+    if (threadIdx.x == 0) y[j] = y[j] / lu[j + (size_t)j * n];
+    __syncthreads();
+    const double yj = y[j];
+    for (int i = threadIdx.x; i < j; i += blockDim.x) y[i] -= lu[i + (size_t)j * n] * yj;
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = y[i];
+}
+
+}  // namespace
+
+void vec_diag_scale(size_t n, double a, const double* d, const double* b, double* x,
+                    cudaStream_t s) {
+  k_diag_scale<<<blocks_for(n), kThreads, 0, s>>>(n, a, d, b, x);
+  FDE_LAUNCH_CHECK();
+}
+void vec_axpy(size_t n, double a, const double* x, double* y, cudaStream_t s) {
+  k_axpy<<<blocks_for(n), kThreads, 0, s>>>(n, a, x, y);
+  FDE_LAUNCH_CHECK();
+}
+void vec_axpy_dev(size_t n, const double* a, double sgn, const double* x, double* y,
+                  cudaStream_t s) {
+  k_axpy_dev<<<blocks_for(n), kThreads, 0, s>>>(n, a, sgn, x, y);
+  FDE_LAUNCH_CHECK();
+}
+void vec_scale_inv_dev(size_t n, const double* a, const double* x, double* y, cudaStream_t s) {
+  k_scale_inv_dev<<<blocks_for(n), kThreads, 0, s>>>(n, a, x, y);
+  FDE_LAUNCH_CHECK();
+}
+void vec_scal(size_t n, double a, double* x, cudaStream_t s) {
+  k_scal<<<blocks_for(n), kThreads, 0, s>>>(n, a, x);
+  FDE_LAUNCH_CHECK();
+}
+void vec_sub(size_t n, const double* x, const double* y, double* out, cudaStream_t s) {
+  k_sub<<<blocks_for(n), kThreads, 0, s>>>(n, x, y, out);
+  FDE_LAUNCH_CHECK();
+}
+void vec_lincomb(size_t n, const double* x0, const double* const* v, const double* c, int k,
+                 double* out, cudaStream_t s) {
+  k_lincomb<<<blocks_for(n), kThreads, 0, s>>>(n, x0, v, c, k, out);
+  FDE_LAUNCH_CHECK();
+}
+
+Reducer::Reducer() : partials_(kMaxBlocks), counter_(1) {
+  FDE_CUDA(cudaMemset(counter_.get(), 0, sizeof(unsigned int)));
+}
+void Reducer::dot(size_t n, const double* x, const double* y, double* out, cudaStream_t s,
+                  bool sqrt_out) {
+  k_dot<<<blocks_for(n), kThreads, 0, s>>>(n, x, y, partials_.get(), counter_.get(), out,
+                                           sqrt_out ? 1 : 0);
+  FDE_LAUNCH_CHECK();
+}
+
+Xfer make_xfer(int n1, int n2, bool cx, bool cy) {
+  Xfer t{};
+  t.n1 = n1;
+  t.n2 = n2;
+  t.k1 = cx ? (n1 - n1 % 2) / 2 : n1;
+  t.k2 = cy ? (n2 - n2 % 2) / 2 : n2;
+  t.par1 = (n1 + 1) % 2;
+  t.par2 = (n2 + 1) % 2;
+  t.cx = cx;
+  t.cy = cy;
+  if (t.k1 == 0 || t.k2 == 0 || (!cx && !cy)) throw InvalidArgument("grid too small to coarsen");
+  return t;
+}
+void xfer_restrict(const Xfer& t, const double* fine, double* coarse, double scale,
+                   cudaStream_t s) {
+  const size_t nc = (size_t)t.k1 * t.k2;
+  k_restrict<<<blocks_for(nc), kThreads, 0, s>>>(t, fine, coarse, scale);
+  FDE_LAUNCH_CHECK();
+}
+void xfer_prolong_add(const Xfer& t, const double* coarse, double* fine, cudaStream_t s) {
+  const size_t nf = (size_t)t.n1 * t.n2;
+  k_prolong<true><<<blocks_for(nf), kThreads, 0, s>>>(t, coarse, fine);
+  FDE_LAUNCH_CHECK();
+}
+void xfer_prolong(const Xfer& t, const double* coarse, double* fine, cudaStream_t s) {
+  const size_t nf = (size_t)t.n1 * t.n2;
+  k_prolong<false><<<blocks_for(nf), kThreads, 0, s>>>(t, coarse, fine);
+  FDE_LAUNCH_CHECK();
+}
+void lu_solve(int n, const double* lu, const int* perm, const double* b, double* x,
+              cudaStream_t s) {
+  k_lu_solve<<<1, 256, (size_t)n * sizeof(double), s>>>(n, lu, perm, b, x);
+  FDE_LAUNCH_CHECK();
+}
+
+}  // namespace fde_b200

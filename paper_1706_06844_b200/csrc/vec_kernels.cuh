@@ -1,0 +1,61 @@
+// Vector, reduction and grid-transfer kernels for the multigrid and Krylov
+// layers (reference: proj/src/kernels.cpp, multigrid.cpp:17-71,160-227,
+// krylov.cpp).  Scalars produced by reductions stay in device memory; the
+// Krylov host loop reads them back in one small copy per iteration.
+#pragma once
+#include "devbuf.cuh"
+
+namespace fde_b200 {
+
+// x = (a * d) .* b                         (zero-guess smoothing, multigrid.cpp:355-356)
+void vec_diag_scale(size_t n, double a, const double* d, const double* b, double* x,
+                    cudaStream_t s);
+// y += a * x                               (kernels::axpy, fma like the AVX2 backend)
+void vec_axpy(size_t n, double a, const double* x, double* y, cudaStream_t s);
+// y += sgn * (*a_dev) * x
+void vec_axpy_dev(size_t n, const double* a_dev, double sgn, const double* x, double* y,
+                  cudaStream_t s);
+// y = x * (1 / *a_dev)                     (v_{i+1} = w / ||w||, krylov.cpp:127-130)
+void vec_scale_inv_dev(size_t n, const double* a_dev, const double* x, double* y,
+                       cudaStream_t s);
+// x *= a
+void vec_scal(size_t n, double a, double* x, cudaStream_t s);
+// out = x - y
+void vec_sub(size_t n, const double* x, const double* y, double* out, cudaStream_t s);
+// out = x0 + sum_k c[k] * v[k]   accumulated in k order (krylov.cpp:136-137,153-155)
+void vec_lincomb(size_t n, const double* x0, const double* const* v_dev, const double* c_dev,
+                 int k, double* out, cudaStream_t s);
+
+// Deterministic two-level dot product: per-block partials + last-block sum in
+// fixed order.  Writes <x,y> to *out_dev (and sqrt to *out_dev if sqrt_out).
+class Reducer {
+ public:
+  Reducer();
+  void dot(size_t n, const double* x, const double* y, double* out_dev, cudaStream_t s,
+           bool sqrt_out = false);
+
+ private:
+  DevBuf<double> partials_;
+  DevBuf<unsigned int> counter_;
+};
+
+// GridTransfer (multigrid.cpp:160-227) between an n1 x n2 fine and a k1 x k2
+// coarse grid; cx/cy select the coarsened directions.
+struct Xfer {
+  int n1, n2, k1, k2, par1, par2, cx, cy;
+};
+Xfer make_xfer(int n1, int n2, bool cx, bool cy);
+// coarse = scale-weighted transpose of prolongation (restrict_full: 0.5,
+// restrict_transpose: 1.0), same operation order as restrict_rows/cols.
+void xfer_restrict(const Xfer& t, const double* fine, double* coarse, double scale,
+                   cudaStream_t s);
+// fine += P coarse (prolong then axpy 1.0, multigrid.cpp:377-378)
+void xfer_prolong_add(const Xfer& t, const double* coarse, double* fine, cudaStream_t s);
+// fine = P coarse
+void xfer_prolong(const Xfer& t, const double* coarse, double* fine, cudaStream_t s);
+
+// x = U^-1 L^-1 P b on one CTA (coarsest CoarseSolve::lu, multigrid.cpp:324-328).
+void lu_solve(int n, const double* lu, const int* perm, const double* b, double* x,
+              cudaStream_t s);
+
+}  // namespace fde_b200

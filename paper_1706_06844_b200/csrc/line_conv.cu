@@ -1,71 +1,137 @@
 // Kernels for the batched Toeplitz line convolutions (see line_conv.cuh).
-#include "line_conv.cuh"
-
+//
+// Per line (length n <= M, L = 2M): three complex length-M transforms --
+// one forward of the packed real input, two inverses of the packed T x and
+// T^T x spectra -- as Stockham radix-16 stages (16 points per thread in
+// registers, plus one radix-2/4/8 stage when log2 M is not a multiple of 4).
+// Shared memory is only the inter-stage exchange buffer, SoA re/im doubles
+// with an XOR swizzle that makes every stage's 8-byte accesses bank-conflict
+// free (half-warp phases).  Stage twiddles cost one table load per butterfly;
+// the other powers come from a depth-4 product tree (the FP64 pipe has the
+// headroom, the L1/shared-memory pipe does not).
 #include <type_traits>
+
+#include "line_conv.cuh"
 
 namespace fde_b200 {
 namespace {
 
-__device__ __forceinline__ int pad(int p) { return p + (p >> 5); }
+__device__ __forceinline__ int swz(int p) { return p ^ ((p >> 4) & 15); }
 
 // ---- small DFTs on registers; INV = false uses exp(-2 pi i / R) -----------
 template <bool INV>
 __device__ __forceinline__ double2 rot90(double2 a) {  // * (-i) forward, * (+i) inverse
   return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
 }
-template <bool INV>
-__device__ __forceinline__ double2 rot45(double2 a) {  // * exp(-+ i pi/4)
+// a * exp(-+ 2 pi i e / 16) for a compile-time exponent e (0..15)
+template <bool INV, int E>
+__device__ __forceinline__ double2 tw16(double2 a) {
+  constexpr int e = E & 15;
+  constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
   constexpr double h = 0.70710678118654752440;
-  return INV ? make_double2((a.x - a.y) * h, (a.x + a.y) * h)
-             : make_double2((a.x + a.y) * h, (a.y - a.x) * h);
-}
-template <bool INV>
-__device__ __forceinline__ double2 rot135(double2 a) {  // * exp(-+ 3 i pi/4)
-  constexpr double h = 0.70710678118654752440;
-  return INV ? make_double2((-a.x - a.y) * h, (a.x - a.y) * h)
-             : make_double2((a.y - a.x) * h, (-a.x - a.y) * h);
+  if constexpr (e == 0) return a;
+  else if constexpr (e == 4) return rot90<INV>(a);
+  else if constexpr (e == 8) return make_double2(-a.x, -a.y);
+  else if constexpr (e == 12) return rot90<!INV>(a);
+  else {
+    // cos and sin of 2 pi e / 16
+    constexpr double cr = e == 1 ? c1 : e == 2 ? h : e == 3 ? s1 : e == 5 ? -s1 : e == 6 ? -h
+                        : e == 7 ? -c1 : e == 9 ? -c1 : e == 10 ? -h : e == 11 ? -s1
+                        : e == 13 ? s1 : e == 14 ? h : c1;
+    constexpr double sn = e == 1 ? s1 : e == 2 ? h : e == 3 ? c1 : e == 5 ? c1 : e == 6 ? h
+                        : e == 7 ? s1 : e == 9 ? -s1 : e == 10 ? -h : e == 11 ? -c1
+                        : e == 13 ? -c1 : e == 14 ? -h : -s1;
+    constexpr double ci = INV ? sn : -sn;  // forward root exp(-i theta)
+    return make_double2(a.x * cr - a.y * ci, a.x * ci + a.y * cr);
+  }
 }
 
-template <int R, bool INV>
+// in place DFT4 of (a0, a1, a2, a3)
+template <bool INV>
+__device__ __forceinline__ void dft4(double2& a0, double2& a1, double2& a2, double2& a3) {
+  const double2 b0 = cadd(a0, a2), b2 = csub(a0, a2);
+  const double2 b1 = cadd(a1, a3), b3 = rot90<INV>(csub(a1, a3));
+  a0 = cadd(b0, b1);
+  a2 = csub(b0, b1);
+  a1 = cadd(b2, b3);
+  a3 = csub(b2, b3);
+}
+
+template <int R, bool INV, bool HALF>
 struct Dft;
-template <bool INV>
-struct Dft<2, INV> {
+template <bool INV, bool HALF>
+struct Dft<2, INV, HALF> {
   __device__ __forceinline__ static void run(double2 (&u)[2]) {
-    const double2 a = u[0], b = u[1];
-    u[0] = cadd(a, b);
-    u[1] = csub(a, b);
+    const double2 t = u[0];
+    u[0] = cadd(t, u[1]);
+    u[1] = csub(t, u[1]);
   }
 };
-template <bool INV>
-struct Dft<4, INV> {
+template <bool INV, bool HALF>
+struct Dft<4, INV, HALF> {
   __device__ __forceinline__ static void run(double2 (&u)[4]) {
-    const double2 a0 = cadd(u[0], u[2]), a2 = csub(u[0], u[2]);
-    const double2 a1 = cadd(u[1], u[3]), a3 = rot90<INV>(csub(u[1], u[3]));
-    u[0] = cadd(a0, a1);
-    u[2] = csub(a0, a1);
-    u[1] = cadd(a2, a3);
-    u[3] = csub(a2, a3);
+    dft4<INV>(u[0], u[1], u[2], u[3]);
   }
 };
-template <bool INV>
-struct Dft<8, INV> {
+template <bool INV, bool HALF>
+struct Dft<8, INV, HALF> {
   __device__ __forceinline__ static void run(double2 (&u)[8]) {
-    const double2 a0 = cadd(u[0], u[4]), a4 = csub(u[0], u[4]);
-    const double2 a1 = cadd(u[1], u[5]), a5 = rot45<INV>(csub(u[1], u[5]));
-    const double2 a2 = cadd(u[2], u[6]), a6 = rot90<INV>(csub(u[2], u[6]));
-    const double2 a3 = cadd(u[3], u[7]), a7 = rot135<INV>(csub(u[3], u[7]));
-    const double2 b0 = cadd(a0, a2), b2 = csub(a0, a2);
-    const double2 b1 = cadd(a1, a3), b3 = rot90<INV>(csub(a1, a3));
-    const double2 b4 = cadd(a4, a6), b6 = csub(a4, a6);
-    const double2 b5 = cadd(a5, a7), b7 = rot90<INV>(csub(a5, a7));
-    u[0] = cadd(b0, b1);
-    u[4] = csub(b0, b1);
-    u[2] = cadd(b2, b3);
-    u[6] = csub(b2, b3);
-    u[1] = cadd(b4, b5);
-    u[5] = csub(b4, b5);
-    u[3] = cadd(b6, b7);
-    u[7] = csub(b6, b7);
+    // radix-2 DIF split, twiddle W8^k, two DFT4s
+    double2 a[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a[k] = cadd(u[k], u[k + 4]);
+      a[k + 4] = csub(u[k], u[k + 4]);
+    }
+    a[5] = tw16<INV, 2>(a[5]);
+    a[6] = tw16<INV, 4>(a[6]);
+    a[7] = tw16<INV, 6>(a[7]);
+    dft4<INV>(a[0], a[1], a[2], a[3]);  // X[0], X[2], X[4], X[6]
+    dft4<INV>(a[4], a[5], a[6], a[7]);  // X[1], X[3], X[5], X[7]
+    u[0] = a[0]; u[2] = a[1]; u[4] = a[2]; u[6] = a[3];
+    u[1] = a[4]; u[3] = a[5]; u[5] = a[6]; u[7] = a[7];
+  }
+};
+// DFT16 = DFT4 (over n2) -> twiddle W16^(n1 k1) -> DFT4 (over n1).
+// HALF: inputs 8..15 are zero (zero-padded forward input, first stage).
+template <bool INV, bool HALF>
+struct Dft<16, INV, HALF> {
+  __device__ __forceinline__ static void run(double2 (&u)[16]) {
+    double2 a[4][4];  // a[n1][k1]
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) {
+      if (HALF) {  // u[n1 + 8] = u[n1 + 12] = 0
+        const double2 x0 = u[n1], x1 = u[n1 + 4];
+        a[n1][0] = cadd(x0, x1);
+        a[n1][2] = csub(x0, x1);
+        const double2 r = rot90<INV>(x1);
+        a[n1][1] = cadd(x0, r);
+        a[n1][3] = csub(x0, r);
+      } else {
+        a[n1][0] = u[n1];
+        a[n1][1] = u[n1 + 4];
+        a[n1][2] = u[n1 + 8];
+        a[n1][3] = u[n1 + 12];
+        dft4<INV>(a[n1][0], a[n1][1], a[n1][2], a[n1][3]);
+      }
+    }
+    a[1][1] = tw16<INV, 1>(a[1][1]);
+    a[1][2] = tw16<INV, 2>(a[1][2]);
+    a[1][3] = tw16<INV, 3>(a[1][3]);
+    a[2][1] = tw16<INV, 2>(a[2][1]);
+    a[2][2] = tw16<INV, 4>(a[2][2]);
+    a[2][3] = tw16<INV, 6>(a[2][3]);
+    a[3][1] = tw16<INV, 3>(a[3][1]);
+    a[3][2] = tw16<INV, 6>(a[3][2]);
+    a[3][3] = tw16<INV, 9>(a[3][3]);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      dft4<INV>(a[0][k1], a[1][k1], a[2][k1], a[3][k1]);
+      u[k1] = a[0][k1];
+      u[k1 + 4] = a[1][k1];
+      u[k1 + 8] = a[2][k1];
+      u[k1 + 12] = a[3][k1];
+    }
   }
 };
 
@@ -74,82 +140,116 @@ struct Log2;
 template <> struct Log2<2> { static constexpr int v = 1; };
 template <> struct Log2<4> { static constexpr int v = 2; };
 template <> struct Log2<8> { static constexpr int v = 3; };
+template <> struct Log2<16> { static constexpr int v = 4; };
 
-// One Stockham stage on NB simultaneous transforms held as v[b][s] =
-// a_b[tl + s*T].  Stage s has radix R and NS = 2^NSL (product of previous
-// radices).  The last stage (NS * R == M) leaves results in registers at the
-// same slots; other stages exchange through shared memory.
-template <int LOGM, bool INV, int NB, int NSL, int R, bool LAST>
-__device__ __forceinline__ void stage(double2 (&v)[NB][8], double* const (&re)[NB],
-                                      double* const (&im)[NB], int tl,
-                                      const double2* twM) {
-  constexpr int M = 1 << LOGM, T = M / 8, NS = 1 << NSL, B = 8 / R;
-  constexpr int TWSH = LOGM - NSL - Log2<R>::v;  // twiddle index = r * jm << TWSH
-#pragma unroll
-  for (int q = 0; q < B; ++q) {
-    const int j = tl + q * T;
-    const int jm = j & (NS - 1);
-    double2 w[R];
-    if (NS > 1) {
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        w[r] = twM[(r * jm) << TWSH];  // plain load: not hoisted across barriers
-        if (INV) w[r].y = -w[r].y;
-      }
-    }
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      double2 u[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) u[r] = v[b][q + r * B];
-      if (NS > 1) {
-#pragma unroll
-        for (int r = 1; r < R; ++r) u[r] = cmul(u[r], w[r]);
-      }
-      Dft<R, INV>::run(u);
-#pragma unroll
-      for (int r = 0; r < R; ++r) v[b][q + r * B] = u[r];
-    }
+// w^r for r = 1..R-1 from w^1 by a shallow product tree (depth <= 4).
+template <int R>
+__device__ __forceinline__ void powers(double2 w1, double2 (&w)[R]) {
+  w[1] = w1;
+  if constexpr (R > 2) {
+    w[2] = cmul(w1, w1);
+    w[3] = cmul(w[2], w1);
   }
-  if (LAST) return;
-  __syncthreads();  // everyone finished reading the previous stage's buffer
-#pragma unroll
-  for (int q = 0; q < B; ++q) {
-    const int j = tl + q * T;
-    const int base = ((j >> NSL) << (NSL + Log2<R>::v)) + (j & (NS - 1));
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int p = pad(base + r * NS);
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        re[b][p] = v[b][q + r * B].x;
-        im[b][p] = v[b][q + r * B].y;
-      }
-    }
+  if constexpr (R > 4) {
+    w[4] = cmul(w[2], w[2]);
+    w[5] = cmul(w[4], w1);
+    w[6] = cmul(w[4], w[2]);
+    w[7] = cmul(w[4], w[3]);
   }
-  __syncthreads();
+  if constexpr (R > 8) {
+    w[8] = cmul(w[4], w[4]);
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    const int p = pad(tl + s * T);
-#pragma unroll
-    for (int b = 0; b < NB; ++b) v[b][s] = make_double2(re[b][p], im[b][p]);
+    for (int r = 9; r < 16; ++r) w[r] = cmul(w[8], w[r - 8]);
   }
 }
 
-// Full length-M transform: radix-8 stages, then one radix-4/2 stage if needed.
-template <int LOGM, bool INV, int NB, int NSL>
+// One Stockham stage on v[s] = a[tl + s*T] (16 slots per thread).  Radix R,
+// NS = 2^NSL.  Non-final stages exchange through shared memory; the final
+// stage leaves results in the same slots.
+// Stage twiddle base W_{NS R}^(j mod NS) for butterfly q (index into exp(-2 pi i k/M)).
+template <int LOGM, int NSL, int R>
+__device__ __forceinline__ void load_tw(double2 (&pre)[16], int tl, const double2* twM) {
+  constexpr int M = 1 << LOGM, T = M / 16, NS = 1 << NSL, B = 16 / R;
+  constexpr int TWSH = LOGM - NSL - Log2<R>::v;
+  if constexpr (NS > 1) {
+#pragma unroll
+    for (int q = 0; q < B; ++q) pre[q] = twM[((tl + q * T) & (NS - 1)) << TWSH];  // plain: stays after the barrier
+  }
+}
+
+template <int LOGM, int NSL>
+struct NextRadix {  // radix of the stage that starts at NSL
+  static constexpr int REM = LOGM - NSL;
+  static constexpr int v = REM >= 4 ? 16 : (REM == 3 ? 8 : (REM == 2 ? 4 : 2));
+};
+
+template <int LOGM, bool INV, int NSL, int R, bool LAST, bool HALF>
+__device__ __forceinline__ void stage(double2 (&v)[16], double* re, double* im, int tl,
+                                      const double2* twM, double2 (&pre)[16]) {
+  constexpr int M = 1 << LOGM, T = M / 16, NS = 1 << NSL, B = 16 / R;
+  // this stage's W^(jm) for each butterfly (loaded before the previous
+  // stage's exchange so the latency hides behind it)
+  double2 tw[B];
+  if (NS > 1) {
+#pragma unroll
+    for (int q = 0; q < B; ++q) tw[q] = pre[q];
+  }
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    const int j = tl + q * T;
+    double2 u[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) u[r] = v[q + r * B];
+    if (NS > 1) {
+      double2 w1 = tw[q];
+      if (INV) w1.y = -w1.y;
+      double2 w[R];
+      powers<R>(w1, w);
+#pragma unroll
+      for (int r = 1; r < R; ++r) u[r] = cmul(u[r], w[r]);
+    }
+    Dft<R, INV, HALF>::run(u);
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[q + r * B] = u[r];
+  }
+  if constexpr (!LAST) {
+    load_tw<LOGM, NSL + Log2<R>::v, NextRadix<LOGM, NSL + Log2<R>::v>::v>(pre, tl, twM);
+    __syncthreads();  // everyone finished reading the previous contents
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const int j = tl + q * T;
+      const int base = ((j >> NSL) << (NSL + Log2<R>::v)) + (j & (NS - 1));
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int p = swz(base + r * NS);
+        re[p] = v[q + r * B].x;
+        im[p] = v[q + r * B].y;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int p = swz(tl + s * T);
+      v[s] = make_double2(re[p], im[p]);
+    }
+  }
+}
+
+// Full length-M transform: radix-16 stages, then one radix-2/4/8 stage.
+template <int LOGM, bool INV, int NSL, bool HALF>
 struct Fft {
-  __device__ __forceinline__ static void run(double2 (&v)[NB][8], double* const (&re)[NB],
-                                             double* const (&im)[NB], int tl,
-                                             const double2* twM) {
+  __device__ __forceinline__ static void run(double2 (&v)[16], double* re, double* im, int tl,
+                                             const double2* twM, double2 (&pre)[16]) {
     constexpr int REM = LOGM - NSL;
-    if constexpr (REM >= 3) {
-      stage<LOGM, INV, NB, NSL, 8, REM == 3>(v, re, im, tl, twM);
-      if constexpr (REM > 3) Fft<LOGM, INV, NB, NSL + 3>::run(v, re, im, tl, twM);
+    if constexpr (REM >= 4) {
+      stage<LOGM, INV, NSL, 16, REM == 4, HALF>(v, re, im, tl, twM, pre);
+      if constexpr (REM > 4) Fft<LOGM, INV, NSL + 4, false>::run(v, re, im, tl, twM, pre);
+    } else if constexpr (REM == 3) {
+      stage<LOGM, INV, NSL, 8, true, false>(v, re, im, tl, twM, pre);
     } else if constexpr (REM == 2) {
-      stage<LOGM, INV, NB, NSL, 4, true>(v, re, im, tl, twM);
+      stage<LOGM, INV, NSL, 4, true, false>(v, re, im, tl, twM, pre);
     } else if constexpr (REM == 1) {
-      stage<LOGM, INV, NB, NSL, 2, true>(v, re, im, tl, twM);
+      stage<LOGM, INV, NSL, 2, true, false>(v, re, im, tl, twM, pre);
     }
   }
 };
@@ -157,12 +257,13 @@ struct Fft {
 template <int LOGM>
 struct FftShape {
   static constexpr int M = 1 << LOGM;
-  static constexpr int T = M / 8;                 // threads per line
-  static constexpr int LPB = T >= 256 ? 1 : 256 / T;  // lines per CTA
+  static constexpr int T = M / 16;                     // threads per line
+  static constexpr int LPB = T >= 128 ? 1 : 128 / T;   // lines per CTA
   static constexpr int THREADS = T * LPB;
-  static constexpr int MINB = THREADS >= 512 ? 1 : 2;  // <= 128 registers per thread
-  static constexpr int MP = M + M / 32;           // padded buffer length (doubles)
-  static constexpr size_t SMEM = size_t(LPB) * 4 * MP * sizeof(double);
+  static constexpr int BUF = M + (T < 16 ? T : 0);     // per-buffer stride (doubles)
+  static constexpr size_t SMEM = size_t(LPB) * 4 * BUF * sizeof(double);
+  // resident CTAs per SM we ask the register allocator for (<= 168 regs)
+  static constexpr int MINB = LOGM == 9 ? 2 : (SMEM * 3 <= 200 * 1024 ? 3 : (SMEM * 2 <= 200 * 1024 ? 2 : 1));
 };
 
 // One CTA convolves LPB lines of length n <= M with T_b and T_b^T.
@@ -170,50 +271,48 @@ template <int LOGM, class P>
 __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
     fft_line_kernel(const P p) {
   using S = FftShape<LOGM>;
-  constexpr int M = S::M, T = S::T, MP = S::MP;
+  constexpr int M = S::M, T = S::T, BUF = S::BUF;
   extern __shared__ double smem[];
   const int ls = threadIdx.x / T, tl = threadIdx.x - ls * T;
   const int line = blockIdx.x * S::LPB + ls;
   const bool active = line < p.nlines();
   const int n = p.blk.n;
-  double* const base = smem + (size_t)ls * 4 * MP;
-  double* const ra[1] = {base};
-  double* const ia[1] = {base + MP};
+  double* const ra = smem + (size_t)ls * 4 * BUF;
+  double* const ia = ra + BUF;
+  double* const rb = ia + BUF;
+  double* const ib = rb + BUF;
 
-  // 1) load the line: z_m = x_2m + i x_2m+1, m = tl + s*T; zero padding
-  //    (n <= M so only s < 4 can be nonzero).
-  double2 v[1][8];
+  // 1) z_m = x_2m + i x_2m+1, m = tl + s*T; zero padded (n <= M: s < 8 only)
+  double2 v[16];
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
+  for (int s = 0; s < 8; ++s) {
     const int i0 = 2 * (tl + s * T);
-    v[0][s].x = (active && i0 < n) ? p.load(line, i0) : 0.0;
-    v[0][s].y = (active && i0 + 1 < n) ? p.load(line, i0 + 1) : 0.0;
-    v[0][s + 4] = make_double2(0.0, 0.0);
+    v[s].x = (active && i0 < n) ? p.load(line, i0) : 0.0;
+    v[s].y = (active && i0 + 1 < n) ? p.load(line, i0 + 1) : 0.0;
+    v[s + 8] = make_double2(0.0, 0.0);
   }
 
-  // 2) forward FFT_M; result in smem (natural order)
-  Fft<LOGM, false, 1, 0>::run(v, ra, ia, tl, p.blk.twM);
+  // 2) forward FFT_M -> Z[tl + s*T] in registers; publish for the partner reads
+  double2 pre[16];
+  Fft<LOGM, false, 0, true>::run(v, ra, ia, tl, p.blk.twM, pre);
   __syncthreads();
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    const int pp = pad(tl + s * T);
-    ra[0][pp] = v[0][s].x;
-    ia[0][pp] = v[0][s].y;
+  for (int s = 0; s < 16; ++s) {
+    const int q = swz(tl + s * T);
+    ra[q] = v[s].x;
+    ia[q] = v[s].y;
   }
   __syncthreads();
 
-  // 3) unpack the real spectrum X[k], X[M-k]; multiply by S and conj(S);
-  //    repack both real outputs for half-length inverse transforms.  The
-  //    T x spectrum stays in registers (stage-0 layout), the T^T x one goes
-  //    to the second buffer.
-  double* const rb[1] = {base + 2 * MP};
-  double* const ib[1] = {base + 3 * MP};
+  // 3) unpack X[k], X[M-k]; Y = X S, Yt = X conj(S); repack both real outputs.
+  //    The T x spectrum stays in registers, the T^T x one goes to buffer b.
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
+  for (int s = 0; s < 16; ++s) {
     const int k = tl + s * T;
     const int km = (M - k) & (M - 1);
-    const double2 zk = make_double2(ra[0][pad(k)], ia[0][pad(k)]);
-    const double2 zm = make_double2(ra[0][pad(km)], ia[0][pad(km)]);
+    const double2 zk = v[s];
+    const int qm = swz(km);
+    const double2 zm = make_double2(ra[qm], ia[qm]);
     const double2 wk = __ldg(&p.blk.twL[k]);
     const double2 pe = cadd(zk, conjg(zm));                    // 2 E[k]
     const double2 po = csub(zk, conjg(zm));                    // 2i O[k]
@@ -225,34 +324,46 @@ __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
     const double2 cw = conjg(wk);
     const double2 yk = cmul(x2k, sk), ym = cmul(x2m, sm);
     const double2 ay = cadd(yk, conjg(ym)), by = cmul(csub(yk, conjg(ym)), cw);
-    v[0][s] = make_double2(ay.x - by.y, ay.y + by.x);  // A + i B
+    v[s] = make_double2(ay.x - by.y, ay.y + by.x);  // A + i B
     const double2 tk = cmul(x2k, conjg(sk)), tm = cmul(x2m, conjg(sm));
     const double2 at = cadd(tk, conjg(tm)), bt = cmul(csub(tk, conjg(tm)), cw);
-    rb[0][pad(k)] = at.x - bt.y;
-    ib[0][pad(k)] = at.y + bt.x;
+    const int qk = swz(k);
+    rb[qk] = at.x - bt.y;
+    ib[qk] = at.y + bt.x;
   }
 
   // 4) unnormalised inverse FFT_M of each packed spectrum -> q = T x (re: even
-  //    positions, im: odd); only m < M/2 (s < 4) carries outputs since n <= M.
-  Fft<LOGM, true, 1, 0>::run(v, ra, ia, tl, p.blk.twM);
-  double2 ty[4];
+  //    positions, im: odd); only m < M/2 (s < 8) carries outputs since n <= M.
+  Fft<LOGM, true, 0, false>::run(v, ra, ia, tl, p.blk.twM, pre);
+  double2 ty[8];
 #pragma unroll
-  for (int s = 0; s < 4; ++s) ty[s] = v[0][s];
+  for (int s = 0; s < 8; ++s) ty[s] = v[s];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    const int pp = pad(tl + s * T);
-    v[0][s] = make_double2(rb[0][pp], ib[0][pp]);
+  for (int s = 0; s < 16; ++s) {
+    const int q = swz(tl + s * T);
+    v[s] = make_double2(rb[q], ib[q]);
   }
-  Fft<LOGM, true, 1, 0>::run(v, rb, ib, tl, p.blk.twM);
+  Fft<LOGM, true, 0, false>::run(v, rb, ib, tl, p.blk.twM, pre);
 
-  // 5) epilogue at the positions the inputs came from (x re-read hits L1/L2)
+  // 5) epilogue at the positions the inputs came from: fetch a group of
+  //    operands, then finish it (one memory latency per group)
   if (!active) return;
+  constexpr int G = 4;
 #pragma unroll
-  for (int s = 0; s < 4; ++s) {
-    const int i0 = 2 * (tl + s * T);
-    if (i0 < n) p.store(line, i0, ty[s].x, v[0][s].x, P::kNeedsX ? p.load(line, i0) : 0.0);
-    if (i0 + 1 < n)
-      p.store(line, i0 + 1, ty[s].y, v[0][s].y, P::kNeedsX ? p.load(line, i0 + 1) : 0.0);
+  for (int g = 0; g < 8; g += G) {
+    typename P::Ops o[2 * G];
+#pragma unroll
+    for (int s = g; s < g + G; ++s) {
+      const int i0 = 2 * (tl + s * T);
+      if (i0 < n) o[2 * (s - g)] = p.fetch(line, i0);
+      if (i0 + 1 < n) o[2 * (s - g) + 1] = p.fetch(line, i0 + 1);
+    }
+#pragma unroll
+    for (int s = g; s < g + G; ++s) {
+      const int i0 = 2 * (tl + s * T);
+      if (i0 < n) p.finish(line, i0, ty[s].x, v[s].x, o[2 * (s - g)]);
+      if (i0 + 1 < n) p.finish(line, i0 + 1, ty[s].y, v[s].y, o[2 * (s - g) + 1]);
+    }
   }
 }
 
@@ -276,7 +387,13 @@ __global__ void __launch_bounds__(256) direct_line_kernel(const P p) {
       tt += b * xk;
     }
   }
-  if (lane < n) p.store(line, lane, ty, tt, xv);
+  if (lane < n) p.finish(line, lane, ty, tt, p.fetch(line, lane));
+  (void)xv;
+}
+
+template <class P>
+int lines_of(const P& p) {
+  return std::is_same<P, YPass>::value ? p.n1 : p.n2;
 }
 
 template <int LOGM, class P>
@@ -288,15 +405,14 @@ void launch_fft(const P& p, cudaStream_t s) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
     configured = true;
   }
-  const int lines = std::is_same<P, YPass>::value ? p.n1 : p.n2;
-  const int grid = (lines + S::LPB - 1) / S::LPB;
+  const int grid = (lines_of(p) + S::LPB - 1) / S::LPB;
   fft_line_kernel<LOGM, P><<<grid, S::THREADS, S::SMEM, s>>>(p);
   FDE_LAUNCH_CHECK();
 }
 
 template <class P>
 void launch_any(const P& p, cudaStream_t s) {
-  const int lines = std::is_same<P, YPass>::value ? p.n1 : p.n2;
+  const int lines = lines_of(p);
   if (lines <= 0) return;
   switch (p.blk.logM) {
     case 0:

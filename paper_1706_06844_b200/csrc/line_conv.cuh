@@ -49,8 +49,15 @@ enum Epilogue : int {
 };
 
 // Column pass: line = x index i, position = y index j (stride n1).
+// Epilogue protocol: fetch(line, pos) issues the plain loads of one output
+// position, finish(...) computes and stores it; the kernel fetches a whole
+// group of positions before finishing any, so one memory latency covers the
+// group (plain loads: ptxas must not hoist them across the stage barriers).
 struct YPass {
   static constexpr bool kNeedsX = false;
+  struct Ops {
+    double ep, em;
+  };
   LineBlockDev blk;
   int n1, n2;
   const double* x;
@@ -62,15 +69,24 @@ struct YPass {
   __device__ __forceinline__ double load(int line, int pos) const {
     return x[(size_t)pos * n1 + line];
   }
-  __device__ __forceinline__ void store(int line, int pos, double ty, double tt, double) const {
+  __device__ __forceinline__ Ops fetch(int line, int pos) const {
     const size_t t = (size_t)line * n2 + pos;
-    q[(size_t)pos * n1 + line] = c * (epT[t] * ty + emT[t] * tt);
+    return Ops{epT[t], emT[t]};
+  }
+  __device__ __forceinline__ void finish(int line, int pos, double ty, double tt,
+                                         const Ops& o) const {
+    q[(size_t)pos * n1 + line] = c * (o.ep * ty + o.em * tt);
   }
 };
 
-// Row pass: line = y index j, position = x index i (contiguous).
+// Row pass: line = y index j, position = x index i (contiguous).  Every
+// thread reads exactly the positions it writes, so the in-place Jacobi update
+// (out == x) has no cross-thread hazard.
 struct XPass {
   static constexpr bool kNeedsX = true;
+  struct Ops {
+    double x, dp, dm, q, e1, e2;
+  };
   LineBlockDev blk;
   int n1, n2;
   const double* x;
@@ -89,19 +105,35 @@ struct XPass {
   __device__ __forceinline__ double load(int line, int pos) const {
     return x[(size_t)line * n1 + pos];
   }
-  __device__ __forceinline__ void store(int line, int pos, double ty, double tt, double xv) const {
+  __device__ __forceinline__ Ops fetch(int line, int pos) const {
+    const size_t p = (size_t)line * n1 + pos;
+    Ops o;
+    o.x = x[p];
+    o.dp = dp[p];
+    o.dm = dm[p];
+    o.q = q ? q[p] : 0.0;
+    o.e1 = epi == EPI_RHS ? src[p] : (epi == EPI_STORE ? 0.0 : b[p]);
+    o.e2 = epi == EPI_JACOBI ? dinv[p] : 0.0;
+    return o;
+  }
+  __device__ __forceinline__ void finish(int line, int pos, double ty, double tt,
+                                         const Ops& o) const {
     const size_t p = (size_t)line * n1 + pos;
     // structured.cpp:128,134-135,146: y = inv_r x; y += s dp t; y += s dm tt; y += Q
-    double y = inv_r * xv;
-    y += sign * dp[p] * ty;
-    y += sign * dm[p] * tt;
-    if (q) y += q[p];
+    double y = inv_r * o.x;
+    y += sign * o.dp * ty;
+    y += sign * o.dm * tt;
+    if (q) y += o.q;
     switch (epi) {
-      case EPI_RHS: out[p] = y + src_scale * src[p]; break;
-      case EPI_RESID: out[p] = b[p] - y; break;
-      case EPI_JACOBI: out[p] = xv + omega * dinv[p] * (b[p] - y); break;
+      case EPI_RHS: out[p] = y + src_scale * o.e1; break;
+      case EPI_RESID: out[p] = o.e1 - y; break;
+      case EPI_JACOBI: out[p] = o.x + omega * o.e2 * (o.e1 - y); break;
       default: out[p] = y; break;
     }
+  }
+  // direct (short-line) kernel convenience
+  __device__ __forceinline__ void store(int line, int pos, double ty, double tt, double) const {
+    finish(line, pos, ty, tt, fetch(line, pos));
   }
 };
 

@@ -203,16 +203,19 @@ class _Checker:
 class Oracle(_Checker):
     prefix = "orc_"
 
-    def _march(self, s, u, its, res, us, wall, solver=0):
-        self._call("march", ctypes.byref(s), solver, _p(u), its.ctypes.data_as(_I), _p(res),
+    _solver = 0
+
+    def _march(self, s, u, its, res, us, wall):
+        self._call("march", ctypes.byref(s), self._solver, _p(u), its.ctypes.data_as(_I), _p(res),
                    _p(us) if us is not None else None, ctypes.byref(wall))
 
     def march(self, s, record=False, solver=0):
+        """solver 0: GMRES(restart) (reference), 1: BiCGSTAB (extension)."""
         self._solver = solver
-        return super().march(s, record)
-
-    def _march_dispatch(self, *a):
-        return self._march(*a, solver=getattr(self, "_solver", 0))
+        try:
+            return super().march(s, record)
+        finally:
+            self._solver = 0
 
     def bicgstab(self, s, b):
         b = np.ascontiguousarray(b, dtype=np.float64)

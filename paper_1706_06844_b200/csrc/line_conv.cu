@@ -16,7 +16,10 @@
 namespace fde_b200 {
 namespace {
 
-__device__ __forceinline__ int swz(int p) { return p ^ ((p >> 4) & 15); }
+// XOR swizzle of the exchange buffers; conflict free for every stage's
+// 8-byte accesses (half-warp phases) when SH = log2(points per thread).
+template <int SH>
+__device__ __forceinline__ int swz(int p) { return p ^ ((p >> SH) & 15); }
 
 // ---- small DFTs on registers; INV = false uses exp(-2 pi i / R) -----------
 template <bool INV>
@@ -76,12 +79,17 @@ struct Dft<4, INV, HALF> {
 template <bool INV, bool HALF>
 struct Dft<8, INV, HALF> {
   __device__ __forceinline__ static void run(double2 (&u)[8]) {
-    // radix-2 DIF split, twiddle W8^k, two DFT4s
+    // radix-2 DIF split, twiddle W8^k, two DFT4s (HALF: inputs 4..7 are zero)
     double2 a[8];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      a[k] = cadd(u[k], u[k + 4]);
-      a[k + 4] = csub(u[k], u[k + 4]);
+      if (HALF) {
+        a[k] = u[k];
+        a[k + 4] = u[k];
+      } else {
+        a[k] = cadd(u[k], u[k + 4]);
+        a[k + 4] = csub(u[k], u[k + 4]);
+      }
     }
     a[5] = tw16<INV, 2>(a[5]);
     a[6] = tw16<INV, 4>(a[6]);
@@ -163,13 +171,10 @@ __device__ __forceinline__ void powers(double2 w1, double2 (&w)[R]) {
   }
 }
 
-// One Stockham stage on v[s] = a[tl + s*T] (16 slots per thread).  Radix R,
-// NS = 2^NSL.  Non-final stages exchange through shared memory; the final
-// stage leaves results in the same slots.
 // Stage twiddle base W_{NS R}^(j mod NS) for butterfly q (index into exp(-2 pi i k/M)).
-template <int LOGM, int NSL, int R>
-__device__ __forceinline__ void load_tw(double2 (&pre)[16], int tl, const double2* twM) {
-  constexpr int M = 1 << LOGM, T = M / 16, NS = 1 << NSL, B = 16 / R;
+template <int LOGM, int P, int NSL, int R>
+__device__ __forceinline__ void load_tw(double2 (&pre)[P], int tl, const double2* twM) {
+  constexpr int M = 1 << LOGM, T = M / P, NS = 1 << NSL, B = P / R;
   constexpr int TWSH = LOGM - NSL - Log2<R>::v;
   if constexpr (NS > 1) {
 #pragma unroll
@@ -177,31 +182,27 @@ __device__ __forceinline__ void load_tw(double2 (&pre)[16], int tl, const double
   }
 }
 
-template <int LOGM, int NSL>
+template <int LOGM, int P, int NSL>
 struct NextRadix {  // radix of the stage that starts at NSL
   static constexpr int REM = LOGM - NSL;
-  static constexpr int v = REM >= 4 ? 16 : (REM == 3 ? 8 : (REM == 2 ? 4 : 2));
+  static constexpr int v = REM >= Log2<P>::v ? P : (1 << REM);
 };
 
-template <int LOGM, bool INV, int NSL, int R, bool LAST, bool HALF>
-__device__ __forceinline__ void stage(double2 (&v)[16], double* re, double* im, int tl,
-                                      const double2* twM, double2 (&pre)[16]) {
-  constexpr int M = 1 << LOGM, T = M / 16, NS = 1 << NSL, B = 16 / R;
-  // this stage's W^(jm) for each butterfly (loaded before the previous
-  // stage's exchange so the latency hides behind it)
-  double2 tw[B];
-  if (NS > 1) {
-#pragma unroll
-    for (int q = 0; q < B; ++q) tw[q] = pre[q];
-  }
+// One Stockham stage on v[s] = a[tl + s*T] (P slots per thread).  Radix R,
+// NS = 2^NSL.  Non-final stages exchange through shared memory; the final
+// stage leaves results in the same slots.
+template <int LOGM, int P, bool INV, int NSL, int R, bool LAST, bool HALF>
+__device__ __forceinline__ void stage(double2 (&v)[P], double* re, double* im, int tl,
+                                      const double2* twM, double2 (&pre)[P]) {
+  constexpr int M = 1 << LOGM, T = M / P, NS = 1 << NSL, B = P / R, SH = Log2<P>::v;
+  (void)M;
 #pragma unroll
   for (int q = 0; q < B; ++q) {
-    const int j = tl + q * T;
     double2 u[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) u[r] = v[q + r * B];
-    if (NS > 1) {
-      double2 w1 = tw[q];
+    if (NS > 1) {  // this stage's W^(jm), loaded before the previous exchange
+      double2 w1 = pre[q];
       if (INV) w1.y = -w1.y;
       double2 w[R];
       powers<R>(w1, w);
@@ -213,7 +214,7 @@ __device__ __forceinline__ void stage(double2 (&v)[16], double* re, double* im, 
     for (int r = 0; r < R; ++r) v[q + r * B] = u[r];
   }
   if constexpr (!LAST) {
-    load_tw<LOGM, NSL + Log2<R>::v, NextRadix<LOGM, NSL + Log2<R>::v>::v>(pre, tl, twM);
+    load_tw<LOGM, P, NSL + Log2<R>::v, NextRadix<LOGM, P, NSL + Log2<R>::v>::v>(pre, tl, twM);
     __syncthreads();  // everyone finished reading the previous contents
 #pragma unroll
     for (int q = 0; q < B; ++q) {
@@ -221,142 +222,153 @@ __device__ __forceinline__ void stage(double2 (&v)[16], double* re, double* im, 
       const int base = ((j >> NSL) << (NSL + Log2<R>::v)) + (j & (NS - 1));
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int p = swz(base + r * NS);
+        const int p = swz<SH>(base + r * NS);
         re[p] = v[q + r * B].x;
         im[p] = v[q + r * B].y;
       }
     }
     __syncthreads();
 #pragma unroll
-    for (int s = 0; s < 16; ++s) {
-      const int p = swz(tl + s * T);
+    for (int s = 0; s < P; ++s) {
+      const int p = swz<SH>(tl + s * T);
       v[s] = make_double2(re[p], im[p]);
     }
   }
 }
 
-// Full length-M transform: radix-16 stages, then one radix-2/4/8 stage.
-template <int LOGM, bool INV, int NSL, bool HALF>
+// Full length-M transform: radix-P stages, then one smaller radix stage.
+template <int LOGM, int P, bool INV, int NSL, bool HALF>
 struct Fft {
-  __device__ __forceinline__ static void run(double2 (&v)[16], double* re, double* im, int tl,
-                                             const double2* twM, double2 (&pre)[16]) {
-    constexpr int REM = LOGM - NSL;
-    if constexpr (REM >= 4) {
-      stage<LOGM, INV, NSL, 16, REM == 4, HALF>(v, re, im, tl, twM, pre);
-      if constexpr (REM > 4) Fft<LOGM, INV, NSL + 4, false>::run(v, re, im, tl, twM, pre);
+  __device__ __forceinline__ static void run(double2 (&v)[P], double* re, double* im, int tl,
+                                             const double2* twM, double2 (&pre)[P]) {
+    constexpr int REM = LOGM - NSL, LP = Log2<P>::v;
+    if constexpr (REM >= LP) {
+      stage<LOGM, P, INV, NSL, P, REM == LP, HALF>(v, re, im, tl, twM, pre);
+      if constexpr (REM > LP) Fft<LOGM, P, INV, NSL + LP, false>::run(v, re, im, tl, twM, pre);
     } else if constexpr (REM == 3) {
-      stage<LOGM, INV, NSL, 8, true, false>(v, re, im, tl, twM, pre);
+      stage<LOGM, P, INV, NSL, 8, true, false>(v, re, im, tl, twM, pre);
     } else if constexpr (REM == 2) {
-      stage<LOGM, INV, NSL, 4, true, false>(v, re, im, tl, twM, pre);
+      stage<LOGM, P, INV, NSL, 4, true, false>(v, re, im, tl, twM, pre);
     } else if constexpr (REM == 1) {
-      stage<LOGM, INV, NSL, 2, true, false>(v, re, im, tl, twM, pre);
+      stage<LOGM, P, INV, NSL, 2, true, false>(v, re, im, tl, twM, pre);
     }
   }
 };
 
+#ifndef FDE_PTS
+#define FDE_PTS 8
+#endif
+#ifndef FDE_MINB_BIG
+#define FDE_MINB_BIG 2
+#endif
+#ifndef FDE_MINB_P8
+#define FDE_MINB_P8 2
+#endif
+
 template <int LOGM>
 struct FftShape {
+  static constexpr int P = FDE_PTS;                    // points per thread
   static constexpr int M = 1 << LOGM;
-  static constexpr int T = M / 16;                     // threads per line
+  static constexpr int T = M / P;                      // threads per line
   static constexpr int LPB = T >= 128 ? 1 : 128 / T;   // lines per CTA
   static constexpr int THREADS = T * LPB;
   static constexpr int BUF = M + (T < 16 ? T : 0);     // per-buffer stride (doubles)
-  static constexpr size_t SMEM = size_t(LPB) * 4 * BUF * sizeof(double);
-  // resident CTAs per SM we ask the register allocator for (<= 168 regs)
-  static constexpr int MINB = LOGM == 9 ? 2 : (SMEM * 3 <= 200 * 1024 ? 3 : (SMEM * 2 <= 200 * 1024 ? 2 : 1));
+  static constexpr size_t SMEM = size_t(LPB) * 2 * BUF * sizeof(double);
+  static constexpr int MINB = THREADS >= 256 ? (P == 8 && THREADS == 256 ? FDE_MINB_P8 : 1)
+                                             : (LOGM == 9 ? 2 : (LOGM >= 10 ? FDE_MINB_BIG : 3));
 };
 
 // One CTA convolves LPB lines of length n <= M with T_b and T_b^T.
-template <int LOGM, class P>
+template <int LOGM, class Pol>
 __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
-    fft_line_kernel(const P p) {
+    fft_line_kernel(const Pol p) {
   using S = FftShape<LOGM>;
-  constexpr int M = S::M, T = S::T, BUF = S::BUF;
+  constexpr int M = S::M, T = S::T, BUF = S::BUF, P = S::P, H = P / 2, SH = Log2<P>::v;
   extern __shared__ double smem[];
   const int ls = threadIdx.x / T, tl = threadIdx.x - ls * T;
   const int line = blockIdx.x * S::LPB + ls;
   const bool active = line < p.nlines();
   const int n = p.blk.n;
-  double* const ra = smem + (size_t)ls * 4 * BUF;
+  double* const ra = smem + (size_t)ls * 2 * BUF;
   double* const ia = ra + BUF;
-  double* const rb = ia + BUF;
-  double* const ib = rb + BUF;
 
-  // 1) z_m = x_2m + i x_2m+1, m = tl + s*T; zero padded (n <= M: s < 8 only)
-  double2 v[16];
+  // 1) z_m = x_2m + i x_2m+1, m = tl + s*T; zero padded (n <= M: s < P/2 only)
+  double2 v[P];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
+  for (int s = 0; s < H; ++s) {
     const int i0 = 2 * (tl + s * T);
     v[s].x = (active && i0 < n) ? p.load(line, i0) : 0.0;
     v[s].y = (active && i0 + 1 < n) ? p.load(line, i0 + 1) : 0.0;
-    v[s + 8] = make_double2(0.0, 0.0);
+    v[s + H] = make_double2(0.0, 0.0);
   }
 
   // 2) forward FFT_M -> Z[tl + s*T] in registers; publish for the partner reads
-  double2 pre[16];
-  Fft<LOGM, false, 0, true>::run(v, ra, ia, tl, p.blk.twM, pre);
+  double2 pre[P];
+#ifndef FDE_EXP_NOFFT
+  Fft<LOGM, P, false, 0, true>::run(v, ra, ia, tl, p.blk.twM, pre);
+#endif
   __syncthreads();
 #pragma unroll
-  for (int s = 0; s < 16; ++s) {
-    const int q = swz(tl + s * T);
+  for (int s = 0; s < P; ++s) {
+    const int q = swz<SH>(tl + s * T);
     ra[q] = v[s].x;
     ia[q] = v[s].y;
   }
   __syncthreads();
 
-  // 3) unpack X[k], X[M-k]; Y = X S, Yt = X conj(S); repack both real outputs.
-  //    The T x spectrum stays in registers, the T^T x one goes to buffer b.
+  // 3) spectral step.  Unpacking the real spectrum X[k], X[M-k] from Z,
+  //    multiplying by S / conj(S) and repacking both real outputs for the
+  //    half-length inverses collapses (per k) to
+  //      Qy[k] = a_k Z[k] + b_k conj(Z[M-k]),  Qt[k] = conj(a_k) Z[k] - conj(b_k) conj(Z[M-k])
+  //    with a_k, b_k precomputed per block (operator.cu): 8 products per k.
+  //    Qy stays in v, Qt in qt (the compiler may keep part of it in
+  //    L1-backed local memory: shared memory stays one buffer per line).
+  double2 qt[P];
 #pragma unroll
-  for (int s = 0; s < 16; ++s) {
+  for (int s = 0; s < P; ++s) {
     const int k = tl + s * T;
-    const int km = (M - k) & (M - 1);
-    const double2 zk = v[s];
-    const int qm = swz(km);
-    const double2 zm = make_double2(ra[qm], ia[qm]);
-    const double2 wk = __ldg(&p.blk.twL[k]);
-    const double2 pe = cadd(zk, conjg(zm));                    // 2 E[k]
-    const double2 po = csub(zk, conjg(zm));                    // 2i O[k]
-    const double2 iwpo = cmul(make_double2(-wk.y, wk.x), po);  // i W^k (2i O[k])
-    const double2 x2k = csub(pe, iwpo);                        // 2 X[k]
-    const double2 x2m = conjg(cadd(pe, iwpo));                 // 2 X[M-k]
-    const double2 sk = __ldg(&p.blk.spec[k]);
-    const double2 sm = __ldg(&p.blk.spec[M - k]);
-    const double2 cw = conjg(wk);
-    const double2 yk = cmul(x2k, sk), ym = cmul(x2m, sm);
-    const double2 ay = cadd(yk, conjg(ym)), by = cmul(csub(yk, conjg(ym)), cw);
-    v[s] = make_double2(ay.x - by.y, ay.y + by.x);  // A + i B
-    const double2 tk = cmul(x2k, conjg(sk)), tm = cmul(x2m, conjg(sm));
-    const double2 at = cadd(tk, conjg(tm)), bt = cmul(csub(tk, conjg(tm)), cw);
-    const int qk = swz(k);
-    rb[qk] = at.x - bt.y;
-    ib[qk] = at.y + bt.x;
+    const int qm = swz<SH>((M - k) & (M - 1));
+    const double zr = v[s].x, zi = v[s].y;
+    const double mr = ra[qm], mi = ia[qm];
+    const double2* abk = reinterpret_cast<const double2*>(p.blk.ab) + 2 * k;
+    const double2 ca = __ldg(abk), cb = __ldg(abk + 1);  // a_k, b_k
+    const double t1 = ca.x * zr, t2 = ca.y * zi, t3 = ca.x * zi, t4 = ca.y * zr;
+    const double u1 = cb.x * mr, u2 = cb.y * mi, u3 = cb.y * mr, u4 = cb.x * mi;
+    v[s] = make_double2((t1 - t2) + (u1 + u2), (t3 + t4) + (u3 - u4));
+    qt[s] = make_double2((t1 + t2) + (u2 - u1), (t3 - t4) + (u3 + u4));
   }
 
   // 4) unnormalised inverse FFT_M of each packed spectrum -> q = T x (re: even
-  //    positions, im: odd); only m < M/2 (s < 8) carries outputs since n <= M.
-  Fft<LOGM, true, 0, false>::run(v, ra, ia, tl, p.blk.twM, pre);
-  double2 ty[8];
+  //    positions, im: odd); only m < M/2 (s < P/2) carries outputs since n <= M.
+#ifndef FDE_EXP_NOFFT
+  Fft<LOGM, P, true, 0, false>::run(v, ra, ia, tl, p.blk.twM, pre);
+#endif
+  double2 ty[H];
 #pragma unroll
-  for (int s = 0; s < 8; ++s) ty[s] = v[s];
+  for (int s = 0; s < H; ++s) ty[s] = v[s];
 #pragma unroll
-  for (int s = 0; s < 16; ++s) {
-    const int q = swz(tl + s * T);
-    v[s] = make_double2(rb[q], ib[q]);
-  }
-  Fft<LOGM, true, 0, false>::run(v, rb, ib, tl, p.blk.twM, pre);
+  for (int s = 0; s < P; ++s) v[s] = qt[s];
+#ifndef FDE_EXP_NOFFT
+  Fft<LOGM, P, true, 0, false>::run(v, ra, ia, tl, p.blk.twM, pre);
+#endif
 
   // 5) epilogue at the positions the inputs came from: fetch a group of
   //    operands, then finish it (one memory latency per group)
   if (!active) return;
-  constexpr int G = 4;
+  constexpr int G = H < 4 ? H : 4;
 #pragma unroll
-  for (int g = 0; g < 8; g += G) {
-    typename P::Ops o[2 * G];
+  for (int g = 0; g < H; g += G) {
+    typename Pol::Ops o[2 * G];
 #pragma unroll
     for (int s = g; s < g + G; ++s) {
       const int i0 = 2 * (tl + s * T);
+#ifdef FDE_EXP_NOEPI
+      o[2 * (s - g)] = typename Pol::Ops{};
+      o[2 * (s - g) + 1] = typename Pol::Ops{};
+#else
       if (i0 < n) o[2 * (s - g)] = p.fetch(line, i0);
       if (i0 + 1 < n) o[2 * (s - g) + 1] = p.fetch(line, i0 + 1);
+#endif
     }
 #pragma unroll
     for (int s = g; s < g + G; ++s) {
@@ -389,6 +401,25 @@ __global__ void __launch_bounds__(256) direct_line_kernel(const P p) {
   }
   if (lane < n) p.finish(line, lane, ty, tt, p.fetch(line, lane));
   (void)xv;
+}
+
+// 32 x 32 tiles, 32 x 8 threads; padded shared tile (8-byte banks).
+__global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict__ in,
+                                                        double* __restrict__ out, int n1, int n2) {
+  __shared__ double tile[32][33];
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    const int i = i0 + tx, j = j0 + ty + k;
+    if (i < n1 && j < n2) tile[ty + k][tx] = in[(size_t)j * n1 + i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    const int j = j0 + tx, i = i0 + ty + k;
+    if (i < n1 && j < n2) out[(size_t)i * n2 + j] = tile[tx][ty + k];
+  }
 }
 
 template <class P>
@@ -433,6 +464,11 @@ void launch_any(const P& p, cudaStream_t s) {
 }  // namespace
 
 void launch_line_pass(const YPass& p, cudaStream_t s) { launch_any(p, s); }
+void launch_transpose(const double* in, double* out, int n1, int n2, cudaStream_t s) {
+  const dim3 grid((n1 + 31) / 32, (n2 + 31) / 32);
+  transpose_kernel<<<grid, 256, 0, s>>>(in, out, n1, n2);
+  FDE_LAUNCH_CHECK();
+}
 void launch_line_pass(const XPass& p, cudaStream_t s) { launch_any(p, s); }
 
 }  // namespace fde_b200

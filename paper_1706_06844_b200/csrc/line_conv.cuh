@@ -34,9 +34,8 @@ constexpr int kDirectMax = 32;  // n <= this: direct Toeplitz product
 struct LineBlockDev {
   int n;                 // line length
   int logM;              // FFT path: M = 2^logM = L/2; 0 -> direct path
-  const double2* spec;   // S[k] / (2L), k = 0..M  (S = DFT_L of the circulant column)
+  const double4* ab;     // per-k spectral constants (a_k, b_k), k < M (operator.cu)
   const double2* twM;    // exp(-2 pi i k / M), k < M
-  const double2* twL;    // exp(-2 pi i k / L), k < M
   const double* col;     // first column, n entries (direct path)
   const double* row;     // first row, n entries (direct path)
 };
@@ -60,14 +59,15 @@ struct YPass {
   };
   LineBlockDev blk;
   int n1, n2;
-  const double* x;
+  const double* x;    // x transposed when xT is set: xT[i * n2 + j] = x[i + j * n1]
+  int xT;
   const double* epT;  // ep transposed: epT[i * n2 + j] = ep[i + j * n1]
   const double* emT;
   double c;           // sign * s_over_r
   double* q;          // Q[i + j * n1]
   __device__ __forceinline__ int nlines() const { return n1; }
   __device__ __forceinline__ double load(int line, int pos) const {
-    return x[(size_t)pos * n1 + line];
+    return xT ? x[(size_t)line * n2 + pos] : x[(size_t)pos * n1 + line];
   }
   __device__ __forceinline__ Ops fetch(int line, int pos) const {
     const size_t t = (size_t)line * n2 + pos;
@@ -138,6 +138,8 @@ struct XPass {
 };
 
 void launch_line_pass(const YPass& p, cudaStream_t s);
+// out[i * n2 + j] = in[i + j * n1] (tiled through shared memory)
+void launch_transpose(const double* in, double* out, int n1, int n2, cudaStream_t s);
 void launch_line_pass(const XPass& p, cudaStream_t s);
 
 }  // namespace fde_b200

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <complex>
 #include <map>
+#include <cstdlib>
 #include <mutex>
 
 #include "operator.cuh"
@@ -78,7 +79,7 @@ void fft_ld(std::vector<cld>& a) {
 }
 
 struct TwiddleTables {
-  DevBuf<double2> twM, twL;
+  DevBuf<double2> twM;
 };
 
 const TwiddleTables& twiddles(int logM) {
@@ -88,14 +89,10 @@ const TwiddleTables& twiddles(int logM) {
   auto& slot = cache[logM];
   if (!slot) {
     const size_t M = size_t(1) << logM;
-    std::vector<double2> tm(M), tl(M);
-    for (size_t k = 0; k < M; ++k) {
-      tm[k] = unit_root(k, M);
-      tl[k] = unit_root(k, 2 * M);
-    }
+    std::vector<double2> tm(M);
+    for (size_t k = 0; k < M; ++k) tm[k] = unit_root(k, M);
     auto t = std::make_unique<TwiddleTables>();
     t->twM.upload(tm.data(), M);
-    t->twL.upload(tl.data(), M);
     slot = std::move(t);
   }
   return *slot;
@@ -126,12 +123,23 @@ ToeplitzDev::ToeplitzDev(std::vector<double> first_col, std::vector<double> firs
   for (size_t i = 0; i < n_; ++i) c[i] = (long double)col_[i];
   for (size_t j = 1; j < n_; ++j) c[L_ - j] = (long double)row_[j];
   fft_ld(c);
-  std::vector<double2> s(M + 1);
+  // Per-k constants of the fused unpack -> multiply -> repack step
+  // (line_conv.cu): with S~ = S / (2L), a = S~[k], b = conj(S~[M-k]),
+  // W = exp(-2 pi i k / L) = cw + i sw:
+  //   a_k = 2 (a + b + sw (a - b)),  b_k = 2 i cw (a - b).
+  std::vector<double4> ab(M);
   const long double sc = 1.0L / (2.0L * (long double)L_);
-  for (size_t k = 0; k <= M; ++k)
-    s[k] = make_double2((double)(c[k].real() * sc), (double)(c[k].imag() * sc));
-  spec_ = std::make_shared<DevBuf<double2>>();
-  spec_->upload(s.data(), s.size());
+  for (size_t k = 0; k < M; ++k) {
+    const cld a = c[k] * sc, b = std::conj(c[M - k] * sc);
+    const long double ang = 2.0L * kPiL * (long double)k / (long double)L_;
+    const long double cw = cosl(ang), sw = -sinl(ang);
+    const cld ak = 2.0L * (a + b + sw * (a - b));
+    const cld bk = 2.0L * cld(0.0L, cw) * (a - b);
+    ab[k] = make_double4((double)ak.real(), (double)ak.imag(), (double)bk.real(),
+                         (double)bk.imag());
+  }
+  spec_ = std::make_shared<DevBuf<double4>>();
+  spec_->upload(ab.data(), ab.size());
 }
 
 ToeplitzDev ToeplitzDev::fractional(double gamma, size_t n, int pq) {
@@ -152,9 +160,8 @@ LineBlockDev ToeplitzDev::dev() const {
   d.row = drow_->get();
   if (logM_) {
     const TwiddleTables& t = twiddles(logM_);
-    d.spec = spec_->get();
+    d.ab = spec_->get();
     d.twM = t.twM.get();
-    d.twL = t.twL.get();
   }
   return d;
 }
@@ -184,6 +191,8 @@ StructuredOp::StructuredOp(size_t n1, size_t n2, double inv_r, double s_over_r,
     diag_[p] = inv_r_ + (dp_[p] + dm_[p]) * ax0 + s_over_r_ * (ep_[p] + em_[p]) * ay0;
   upload();
   d_q_.alloc(n);
+  d_xT_.alloc(n);
+  if (const char* e = std::getenv("FDE_NO_TRANSPOSE")) transpose_columns_ = e[0] != '1';
 }
 
 void StructuredOp::upload() {
@@ -219,6 +228,12 @@ void StructuredOp::run(const double* x, double* out, double sign, int epi, const
   yp.n1 = (int)n1_;
   yp.n2 = (int)n2_;
   yp.x = x;
+  // FFT-path columns read a transposed copy (coalesced) instead of stride-n1 gathers
+  if (yp.blk.logM && n1_ > 1 && transpose_columns_) {
+    launch_transpose(x, d_xT_.get(), (int)n1_, (int)n2_, s);
+    yp.x = d_xT_.get();
+    yp.xT = 1;
+  }
   yp.epT = d_epT_.get();
   yp.emT = d_emT_.get();
   yp.c = sign * s_over_r_;

@@ -44,7 +44,7 @@ class ToeplitzDev {
   size_t n_ = 0, L_ = 0;
   int logM_ = 0;
   std::vector<double> col_, row_;
-  std::shared_ptr<DevBuf<double2>> spec_;
+  std::shared_ptr<DevBuf<double4>> spec_;  // per-k spectral constants
   std::shared_ptr<DevBuf<double>> dcol_, drow_;
 };
 
@@ -90,7 +90,8 @@ class StructuredOp {
   ToeplitzDev ax_, ay_;
   std::vector<double> dp_, dm_, ep_, em_, diag_;
   DevBuf<double> d_dp_, d_dm_, d_epT_, d_emT_, d_diag_;
-  mutable DevBuf<double> d_q_;
+  mutable DevBuf<double> d_q_, d_xT_;
+  bool transpose_columns_ = true;
 };
 
 }  // namespace fde_b200

@@ -180,22 +180,21 @@ KrylovResult KrylovWorkspace::gmres(const StructuredOp& a, const Precond* m,
     for (size_t i = 0; i < rst && !cycle_done; ++i) {
       a.apply(v_[i].get(), t_.get(), s);
       precondition(m, t_.get(), w_.get(), s);
-      red_.dot(n, w_.get(), w_.get(), dnorm0, s, true);
-      for (size_t k = 0; k <= i; ++k) {  // modified Gram-Schmidt
-        red_.dot(n, v_[k].get(), w_.get(), dh + k, s);
-        vec_axpy_dev(n, dh + k, -1.0, v_[k].get(), w_.get(), s);
-      }
-      red_.dot(n, w_.get(), w_.get(), dnrmw, s, true);
+      // modified Gram-Schmidt (krylov.cpp:92-97), each subtraction fused with
+      // the next projection: i + 2 passes over w instead of 2 (i + 1) + 2
+      red_.norm_dot(n, w_.get(), v_[0].get(), dnorm0, dh, s);
+      for (size_t k = 0; k <= i; ++k)
+        red_.mgs(n, w_.get(), v_[k].get(), dh + k, k < i ? v_[k + 1].get() : w_.get(),
+                 k < i ? dh + k + 1 : dnrmw, k == i, s);
       fetch(ld + 2, s);
       for (size_t k = 0; k <= i; ++k) h[i * ld + k] = hsc_[k];
       const double norm0 = hsc_[ld];
       double hip = hsc_[ld + 1];
       if (hip < 1e-8 * norm0) {  // second pass (krylov.cpp:98-104)
-        for (size_t k = 0; k <= i; ++k) {
-          red_.dot(n, v_[k].get(), w_.get(), dreo + k, s);
-          vec_axpy_dev(n, dreo + k, -1.0, v_[k].get(), w_.get(), s);
-        }
-        red_.dot(n, w_.get(), w_.get(), dnrmw, s, true);
+        red_.dot(n, v_[0].get(), w_.get(), dreo, s);
+        for (size_t k = 0; k <= i; ++k)
+          red_.mgs(n, w_.get(), v_[k].get(), dreo + k, k < i ? v_[k + 1].get() : w_.get(),
+                   k < i ? dreo + k + 1 : dnrmw, k == i, s);
         fetch(ld + 2 + i + 1, s);
         for (size_t k = 0; k <= i; ++k) h[i * ld + k] += hsc_[ld + 2 + k];
         hip = hsc_[ld + 1];

@@ -229,7 +229,7 @@ void StructuredOp::run(const double* x, double* out, double sign, int epi, const
   yp.n2 = (int)n2_;
   yp.x = x;
   // FFT-path columns read a transposed copy (coalesced) instead of stride-n1 gathers
-  if (yp.blk.logM && n1_ > 1 && transpose_columns_) {
+  if (yp.blk.logM && n1_ >= 512 && transpose_columns_) {
     launch_transpose(x, d_xT_.get(), (int)n1_, (int)n2_, s);
     yp.x = d_xT_.get();
     yp.xT = 1;

@@ -89,6 +89,85 @@ __global__ void k_dot(size_t n, const double* __restrict__ x, const double* __re
   }
 }
 
+// Last-block finalisation shared by the fused reductions: block partial v of
+// reduction r lands in partials[r * kMaxBlocks + block]; the last block to
+// arrive sums each reduction's partials in block order (deterministic).
+template <int NR>
+__device__ __forceinline__ void reduce_finish(double (&v)[NR], double* partials,
+                                              unsigned int* counter, double* const (&out)[NR],
+                                              const int (&sqrt_out)[NR]) {
+  __shared__ double ws[NR][kThreads / 32];
+  __shared__ bool last;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const double t = warp_sum(v[r]);
+    if ((threadIdx.x & 31) == 0) ws[r][threadIdx.x >> 5] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      double t = 0.0;
+      for (int w = 0; w < kThreads / 32; ++w) t += ws[r][w];
+      partials[r * kMaxBlocks + blockIdx.x] = t;
+    }
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    double t = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
+      t += ((volatile double*)partials)[r * kMaxBlocks + b];
+    t = warp_sum(t);
+    if ((threadIdx.x & 31) == 0) ws[r][threadIdx.x >> 5] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      double t = 0.0;
+      for (int w = 0; w < kThreads / 32; ++w) t += ws[r][w];
+      *out[r] = sqrt_out[r] ? sqrt(t) : t;
+    }
+    *counter = 0u;
+  }
+}
+
+// out0 = ||w|| (sqrt of <w,w>), out1 = <v, w> in one pass over w (MGS start).
+__global__ void k_norm_dot(size_t n, const double* __restrict__ w, const double* __restrict__ v,
+                           double* partials, unsigned int* counter, double* out0, double* out1) {
+  double acc[2] = {0.0, 0.0};
+  GRID_STRIDE(i, n) {
+    const double wi = w[i];
+    acc[0] = fma(wi, wi, acc[0]);
+    acc[1] = fma(v[i], wi, acc[1]);
+  }
+  double* const outs[2] = {out0, out1};
+  const int sq[2] = {1, 0};
+  reduce_finish<2>(acc, partials, counter, outs, sq);
+}
+
+// One modified Gram-Schmidt step fused with the next projection:
+//   w -= (*hk) v_k;  *out = <v_next, w>   (v_next == w: *out = ||w||)
+__global__ void k_mgs(size_t n, double* __restrict__ w, const double* __restrict__ vk,
+                      const double* __restrict__ hk, const double* vnext, double* partials,
+                      unsigned int* counter, double* out, int sqrt_out) {
+  const double h = -*hk;
+  double acc[1] = {0.0};
+  GRID_STRIDE(i, n) {
+    const double wi = fma(h, vk[i], w[i]);  // kernels::axpy(-h, v_k, w) (AVX2 fma)
+    w[i] = wi;
+    acc[0] = fma(vnext == w ? wi : vnext[i], wi, acc[0]);
+  }
+  double* const outs[1] = {out};
+  const int sq[1] = {sqrt_out};
+  reduce_finish<1>(acc, partials, counter, outs, sq);
+}
+
 // ---- grid transfers ---------------------------------------------------------
 // restrict_rows (multigrid.cpp:46-58): v = f[fc]; v += .5 f[fc-1]; v += .5 f[fc+1]; scale*v
 __device__ __forceinline__ double rrow(const double* f, int n, int fc, double sc) {
@@ -230,13 +309,26 @@ void vec_lincomb(size_t n, const double* x0, const double* const* v, const doubl
   FDE_LAUNCH_CHECK();
 }
 
-Reducer::Reducer() : partials_(kMaxBlocks), counter_(1) {
+Reducer::Reducer() : partials_(2 * kMaxBlocks), counter_(1) {
   FDE_CUDA(cudaMemset(counter_.get(), 0, sizeof(unsigned int)));
 }
 void Reducer::dot(size_t n, const double* x, const double* y, double* out, cudaStream_t s,
                   bool sqrt_out) {
   k_dot<<<blocks_for(n), kThreads, 0, s>>>(n, x, y, partials_.get(), counter_.get(), out,
                                            sqrt_out ? 1 : 0);
+  FDE_LAUNCH_CHECK();
+}
+
+void Reducer::norm_dot(size_t n, const double* w, const double* v, double* norm_out,
+                       double* dot_out, cudaStream_t s) {
+  k_norm_dot<<<blocks_for(n), kThreads, 0, s>>>(n, w, v, partials_.get(), counter_.get(),
+                                                norm_out, dot_out);
+  FDE_LAUNCH_CHECK();
+}
+void Reducer::mgs(size_t n, double* w, const double* vk, const double* hk, const double* vnext,
+                  double* out, bool sqrt_out, cudaStream_t s) {
+  k_mgs<<<blocks_for(n), kThreads, 0, s>>>(n, w, vk, hk, vnext, partials_.get(),
+                                           counter_.get(), out, sqrt_out ? 1 : 0);
   FDE_LAUNCH_CHECK();
 }
 

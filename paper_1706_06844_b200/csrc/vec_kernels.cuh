@@ -33,6 +33,12 @@ class Reducer {
   Reducer();
   void dot(size_t n, const double* x, const double* y, double* out_dev, cudaStream_t s,
            bool sqrt_out = false);
+  // *norm_out = ||w||, *dot_out = <v, w> in one pass (first MGS projection)
+  void norm_dot(size_t n, const double* w, const double* v, double* norm_out, double* dot_out,
+                cudaStream_t s);
+  // w -= (*hk) v_k, then *out = <v_next, w> (sqrt when sqrt_out; v_next may be w)
+  void mgs(size_t n, double* w, const double* vk, const double* hk, const double* vnext,
+           double* out, bool sqrt_out, cudaStream_t s);
 
  private:
   DevBuf<double> partials_;

@@ -256,7 +256,7 @@ struct Fft {
 };
 
 #ifndef FDE_PTS
-#define FDE_PTS 8
+#define FDE_PTS 16
 #endif
 #ifndef FDE_MINB_BIG
 #define FDE_MINB_BIG 2

@@ -1,5 +1,6 @@
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <utility>
 
 #include "krylov.cuh"
@@ -64,6 +65,21 @@ Precond::Precond(int kind, std::shared_ptr<Hierarchy> h, size_t n, size_t cycles
     : kind_(kind), h_(std::move(h)), n_(n), cycles_(cycles) {
   if (kind_ != PC_NONE && !h_) throw InvalidArgument("preconditioner needs a hierarchy");
   if (kind_ != PC_NONE && cycles_ == 0) throw InvalidArgument("cycles must be >= 1");
+  if (const char* e = std::getenv("FDE_NO_GRAPH")) use_graphs_ = e[0] != '1';
+}
+
+Precond::~Precond() {
+  for (Entry& e : graphs_) cudaGraphExecDestroy(e.exec);
+  if (cap_) cudaStreamDestroy(cap_);
+}
+
+void Precond::record(const double* r, double* z, cudaStream_t s) const {
+  // z = 0; cycles x vcycle(r, z): the first cycle is the zero-guess path
+  // (the reference scans z, multigrid.cpp:387-392).  With one cycle the
+  // zero fill is dead work: every path of the zero-guess cycle writes z.
+  if (cycles_ > 1 || h_->coarse() == COARSE_NONE)
+    FDE_CUDA(cudaMemsetAsync(z, 0, n_ * sizeof(double), s));
+  for (size_t c = 0; c < cycles_; ++c) h_->vcycle(r, z, c == 0, s);
 }
 
 void Precond::apply(const double* r, double* z, cudaStream_t s) const {
@@ -71,12 +87,39 @@ void Precond::apply(const double* r, double* z, cudaStream_t s) const {
     FDE_CUDA(cudaMemcpyAsync(z, r, n_ * sizeof(double), cudaMemcpyDeviceToDevice, s));
     return;
   }
-  // z = 0; cycles x vcycle(r, z): the first cycle is the zero-guess path
-  // (the reference scans z, multigrid.cpp:387-392).  With one cycle the
-  // zero fill is dead work: every path of the zero-guess cycle writes z.
-  if (cycles_ > 1 || h_->coarse() == COARSE_NONE)
-    FDE_CUDA(cudaMemsetAsync(z, 0, n_ * sizeof(double), s));
-  for (size_t c = 0; c < cycles_; ++c) h_->vcycle(r, z, c == 0, s);
+  if (!use_graphs_) {
+    record(r, z, s);
+    return;
+  }
+  for (const Entry& e : graphs_)
+    if (e.r == r && e.z == z) {
+      FDE_CUDA(cudaGraphLaunch(e.exec, s));
+      g_kernel_launches.fetch_add(e.kernels, std::memory_order_relaxed);
+      return;
+    }
+  if (graphs_.size() >= 8) {  // bounded cache (callers normally reuse a few buffers)
+    for (Entry& e : graphs_) cudaGraphExecDestroy(e.exec);
+    graphs_.clear();
+  }
+  if (!cap_) FDE_CUDA(cudaStreamCreateWithFlags(&cap_, cudaStreamNonBlocking));
+  cudaGraph_t g = nullptr;
+  const unsigned long long before = g_kernel_launches.load();
+  FDE_CUDA(cudaStreamBeginCapture(cap_, cudaStreamCaptureModeRelaxed));
+  try {
+    record(r, z, cap_);
+  } catch (...) {
+    cudaStreamEndCapture(cap_, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  FDE_CUDA(cudaStreamEndCapture(cap_, &g));
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t err = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  FDE_CUDA(err);
+  // captured launches were counted while recording; replays count again
+  graphs_.push_back(Entry{r, z, exec, g_kernel_launches.load() - before});
+  FDE_CUDA(cudaGraphLaunch(exec, s));
 }
 
 KrylovWorkspace::KrylovWorkspace(size_t n, size_t restart) : n_(n), rst_(restart) {

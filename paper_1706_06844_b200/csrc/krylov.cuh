@@ -21,16 +21,31 @@ enum PrecondKind : int { PC_NONE = 0, PC_P2 = 1, PC_MGM = 2 };
 class Precond {
  public:
   Precond(int kind, std::shared_ptr<Hierarchy> h, size_t n, size_t cycles);
+  ~Precond();
+  Precond(const Precond&) = delete;
+  Precond& operator=(const Precond&) = delete;
   int kind() const { return kind_; }
   size_t size() const { return n_; }
   const Hierarchy* hierarchy() const { return h_.get(); }
   // z = cycles V-cycles from z = 0 (precond.cpp:22-26); PC_NONE copies.
+  // The whole cycle (~7 launches per level) is captured once per (r, z)
+  // pair into a CUDA graph and replayed (FDE_NO_GRAPH=1 disables).
   void apply(const double* r, double* z, cudaStream_t s) const;
 
  private:
+  void record(const double* r, double* z, cudaStream_t s) const;
   int kind_;
   std::shared_ptr<Hierarchy> h_;
   size_t n_, cycles_;
+  bool use_graphs_ = true;
+  mutable cudaStream_t cap_ = nullptr;
+  struct Entry {
+    const double* r;
+    double* z;
+    cudaGraphExec_t exec;
+    unsigned long long kernels;  // kernel nodes, for fde_kernel_launches()
+  };
+  mutable std::vector<Entry> graphs_;
 };
 
 struct SolverConfig {  // krylov.hpp:16-21

@@ -5,7 +5,8 @@ operator-apply GB/s -- BASELINE.json's metric on configs[3] (cfg4).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
 Own arm (default): one rank per GPU (torchrun for N>1).  A "step" is one
-CN-WSGD time step of cfg4 (n1=n2=2047, alpha=1.6, beta=1.4, tau=1/64,
+CN-WSGD time step of cfg4 (the march continues past cfg4's 8 steps with
+the same tau when W + K > 8; every step is the same work) (n1=n2=2047, alpha=1.6, beta=1.4, tau=1/64,
 config-2 coefficients, seeded U[0,1) source, GMRES(20)+V-cycle mgm,
 omega=0.7, 3 coarsest sweeps, tol 1e-8) through the library's public step
 API.  `value`: inputs (per-step sources) resident in HBM before the timed
@@ -85,6 +86,7 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index, self.proc, self.rows = index, None, []
+        self.t0, self.t1 = 0.0, float("inf")
 
     def start(self):
         try:
@@ -93,7 +95,7 @@ class ClockSampler:
                  "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except OSError:
@@ -101,7 +103,11 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.rows.append((time.time(), [c.strip() for c in line.split(",")]))
+
+    def window(self, t0, t1):
+        """Keep only samples taken inside the timed region [t0, t1]."""
+        self.t0, self.t1 = t0, t1
 
     def stop(self):
         if self.proc is None:
@@ -112,7 +118,8 @@ class ClockSampler:
         except subprocess.TimeoutExpired:
             self.proc.kill()
         time.sleep(0.05)
-        rows = [r for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        rows = [r for t, r in self.rows if self.t0 <= t <= self.t1 + 0.06
+                and len(r) >= 8 and r[0].replace(".", "").isdigit()]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
         sm = [float(r[0]) for r in rows]
@@ -140,12 +147,12 @@ def run_reference(args):
     # each reported step is one real cfg4 time step of the reference, run with
     # its own time_march on 1 core; a bounded sample of the K+W requested
     # steps keeps the run to a few minutes (~40-70 s per step).
-    nsteps = max(1, min(args.steps, int(os.environ.get("FDE_REF_STEPS", "1"))))
+    nsteps = max(1, min(args.steps, int(os.environ.get("FDE_REF_STEPS", "2"))))
     s = spec(CFG, steps=nsteps, tau=TAU)
     t0 = time.perf_counter()
     if kind == "reference":
-        r = lib.time_march(s)
-        wall = r["wall"]
+        r = lib.march_timed(s)  # the reference's own assemble_rhs + gmres per step
+        wall = float(np.sum(r["step_seconds"]))
     else:
         r = lib.march(s)
         wall = r["wall"]
@@ -159,9 +166,10 @@ def run_reference(args):
         "config": dict(CONFIG, sample=f"{nsteps} real time step(s) m=1..{nsteps} of cfg4"),
         "iterations_per_step": [int(v) for v in r["its"]],
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind,
-                         "sample": f"{nsteps} full reference time_march step(s) of cfg4 "
-                                   f"(single-threaded, the reference's native mode; "
-                                   f"wall incl. setup {total:.1f} s)"},
+                         "sample": f"{nsteps} full reference time steps of cfg4 (assemble_rhs + "
+                                   f"gmres with the mgm V-cycle, driver.cpp:34-52), timed per "
+                                   f"step excluding the one-off setup; single-threaded, the "
+                                   f"reference's native mode; whole run {total:.1f} s"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -220,12 +228,14 @@ def run_own(args):
     march = fde.March(prob, N, N, total, cfg)
     srcs = [torch.tensor(prob.sample_source(N, N, total, m), device=dev) for m in range(1, total + 1)]
     log(f"[bench] setup {time.perf_counter() - t_setup:.1f} s")
+    clk = ClockSampler(local)
+    clk.start()  # running through the warm-up; only samples inside the timed window count
     its = []
     for m in range(args.warmup):
         its.append(march.step(srcs[m])[0])
+    time.sleep(0.3)
     barrier()
-    clk = ClockSampler(local)
-    clk.start()
+    t_start = time.time()
     launches0 = fde.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -234,6 +244,7 @@ def run_own(args):
         timed_its.append(march.step(srcs[m])[0])
     e1.record(stream)
     barrier()
+    clk.window(t_start, time.time())
     clocks = clk.stop()
     launches = fde.kernel_launches() - launches0
     ms = e0.elapsed_time(e1)
@@ -336,7 +347,7 @@ def run_own(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

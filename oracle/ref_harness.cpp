@@ -495,8 +495,17 @@ int ref_gmres(const ref_spec* s, const double* b, double* x, int* iterations, in
 
 // Per-step time march (driver.cpp:34-52 over reference assemble_rhs/gmres),
 // recording every u^m when u_steps != NULL.
+int ref_march_timed(const ref_spec* s, double* u_out, int* its, double* res, double* u_steps,
+                    double* wall, double* step_seconds);
+
 int ref_march(const ref_spec* s, double* u_out, int* its, double* res, double* u_steps,
               double* wall) {
+  return ref_march_timed(s, u_out, its, res, u_steps, wall, nullptr);
+}
+
+// Same loop; step_seconds[m-1] = wall time of step m alone (rhs + gmres).
+int ref_march_timed(const ref_spec* s, double* u_out, int* its, double* res, double* u_steps,
+                    double* wall, double* step_seconds) {
   return guarded([&] {
     const Setup st = make_setup(*s);
     const auto t0 = std::chrono::steady_clock::now();
@@ -510,8 +519,12 @@ int ref_march(const ref_spec* s, double* u_out, int* its, double* res, double* u
     c.preconditioner = pc.get();
     const std::size_t n = st.g.size();
     for (std::size_t m = 1; m <= st.g.steps; ++m) {
+      const auto ts = std::chrono::steady_clock::now();
       const std::vector<double> b = fde::assemble_rhs(st.p, st.g, m, u, op);
       fde::KrylovResult r = fde::gmres(op, c, b);
+      if (step_seconds)
+        step_seconds[m - 1] =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - ts).count();
       its[m - 1] = static_cast<int>(r.total_iterations);
       res[m - 1] = r.residual_history.back();
       u = std::move(r.solution);
@@ -526,8 +539,8 @@ int ref_march(const ref_spec* s, double* u_out, int* its, double* res, double* u
 // The reference's own fde::time_march (driver.cpp:10-69), (1,0) weights only.
 int ref_time_march(const ref_spec* s, double* u_out, int* its, double* res, double* wall) {
   return guarded([&] {
-    if (s->pq != 0) throw std::invalid_argument("time_march supports (p,q)=(1,0) only");
     const Setup st = make_setup(*s);
+    if (st.pq != 0) throw std::invalid_argument("time_march supports (p,q)=(1,0) only");
     fde::DriverConfig c;
     c.precond = s->precond == 2 ? fde::PrecondKind::mgm
                                 : (s->precond == 1 ? fde::PrecondKind::p2 : fde::PrecondKind::none);

@@ -69,12 +69,13 @@ class _Checker:
 
     def __init__(self, path: Path):
         self.lib = ctypes.CDLL(str(path))
-        self.lib[f"{self.prefix}last_error"].restype = ctypes.c_char_p
+        getattr(self.lib, f"{self.prefix}last_error").restype = ctypes.c_char_p
 
     def _call(self, name, *args):
-        rc = self.lib[self.prefix + name](*args)
+        rc = getattr(self.lib, self.prefix + name)(*args)
         if rc != 0:
-            raise RuntimeError(f"{self.prefix}{name}: {self.lib[self.prefix + 'last_error']().decode()}")
+            msg = getattr(self.lib, self.prefix + "last_error")()
+            raise RuntimeError(f"{self.prefix}{name}: {msg.decode() if msg else rc}")
         return rc
 
     def weights(self, gamma, K, pq=0):
@@ -244,6 +245,16 @@ class RefLib(_Checker):
     def _march(self, s, u, its, res, us, wall):
         self._call("march", ctypes.byref(s), _p(u), its.ctypes.data_as(_I), _p(res),
                    _p(us) if us is not None else None, ctypes.byref(wall))
+
+    def march_timed(self, s):
+        """Per-step loop of time_march with per-step wall times (setup excluded)."""
+        n1, n2 = dims_of(s)
+        steps = s.steps or CONFIGS[s.cfg][4]
+        u, its, res = np.zeros(n1 * n2), np.zeros(steps, np.int32), np.zeros(steps)
+        sec, wall = np.zeros(steps), ctypes.c_double()
+        self._call("march_timed", ctypes.byref(s), _p(u), its.ctypes.data_as(_I), _p(res), None,
+                   ctypes.byref(wall), _p(sec))
+        return dict(u=u, its=its, res=res, step_seconds=sec, wall=wall.value)
 
     def time_march(self, s):
         n1, n2 = dims_of(s)

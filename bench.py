@@ -223,6 +223,9 @@ def run_own(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
+    if world > 1:
+        return run_own_distributed(args, prob, cfg, rank, world, local, dev, stream, barrier)
+
     # ---- value: sources resident in HBM
     t_setup = time.perf_counter()
     march = fde.March(prob, N, N, total, cfg)
@@ -341,6 +344,56 @@ def run_own(args):
         print(json.dumps(out), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+    return 0
+
+
+def run_own_distributed(args, prob, cfg, rank, world, local, dev, stream, barrier):
+    """N > 1: y-slab decomposition (paper_1706_06844_b200.distributed) over NCCL;
+    every rank owns n/N grid rows; steps/s of the whole job (max over ranks)."""
+    import torch
+    import paper_1706_06844_b200 as fde
+    from paper_1706_06844_b200 import distributed as D
+
+    total = args.warmup + args.steps
+    ctx = D.DistContext(rank, world, D.GpuBackend(dev))
+    march = D.DistMarch(ctx, prob, N, N, total, tol=cfg.tol, restart=cfg.restart,
+                        max_outer=cfg.max_outer, omega=cfg.omega, coarse=cfg.coarse,
+                        coarse_sweeps=cfg.coarse_sweeps)
+    lv = march.level
+    srcs = [torch.tensor(prob.sample_source(N, N, total, m)[lv.r0 * N:lv.r1 * N], device=dev)
+            for m in range(1, total + 1)]
+    its = [march.step(srcs[m])[0] for m in range(args.warmup)]
+    barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    barrier()
+    t_start = time.time()
+    launches0 = fde.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    timed = [march.step(srcs[m])[0] for m in range(args.warmup, total)]
+    e1.record(stream)
+    barrier()
+    clk.window(t_start, time.time())
+    clocks = clk.stop()
+    ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    torch.distributed.all_reduce(ms, op=torch.distributed.ReduceOp.MAX)
+    ms = float(ms.item())
+    out = {
+        "metric": METRIC, "value": args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-hash U[0,1) source, SURVEY Appendix A)",
+        "config": dict(CONFIG, parallelism=f"y-slab x{world} (NCCL all-to-all transposes, "
+                                         f"ordered all-gather dots, replicated coarse tail)"),
+        "iterations_per_step": [int(v) for v in timed], "warmup_iterations": [int(v) for v in its],
+        "gpu_launches": int(fde.kernel_launches() - launches0), "clocks": clocks,
+        "e2e": None,
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    torch.distributed.destroy_process_group()
     return 0
 
 

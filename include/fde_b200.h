@@ -211,6 +211,54 @@ int fde_time_march(const fde_problem* p, size_t n1, size_t n2, size_t steps,
                    const fde_driver_config* cfg, double* solution, size_t* step_iterations,
                    double* step_residuals, double* wall_seconds);
 
+/* ------------------------------------------------ multi-GPU building blocks
+ * y-slab decomposition.  A slab is rank r's piece of a level
+ * operator (d1 x d2 grid of problem p at step m, rescaled onto the fine
+ * nf1 x nf2 level like build_geometric_hierarchy): rows [r0, r1) for the row
+ * pass and columns [c0, c1) for the column pass.  The caller moves data
+ * between the two layouts (all-to-all); these entry points are the local
+ * compute.  Device arrays. */
+typedef struct fde_slab_s* fde_slab;
+int fde_slab_create(const fde_problem* p, size_t nf1, size_t nf2, size_t d1, size_t d2,
+                    size_t steps, size_t m, size_t r0, size_t r1, size_t c0, size_t c1,
+                    fde_slab* out);
+/* QT[c * d2 + j] = sign * s/r * (ep T_b x + em T_b^T x) at column c0 + c, from
+ * xT[c * d2 + j] = x[(c0 + c) + j * d1] */
+int fde_slab_ypass(fde_slab h, const double* xT, double* QT, double sign, void* stream);
+/* rows r0..r1 (local row-major blocks of width d1): out = epilogue(inv_r x +
+ * sign (dp T_a x + dm T_a^T x) + Q); epi 0 store, 1 rhs (+ src_scale src),
+ * 2 residual (b - .), 3 Jacobi (x + omega dinv (b - .)) */
+int fde_slab_xpass(fde_slab h, const double* x, const double* Q, double* out, double sign,
+                   int epi, const double* b, const double* dinv, double omega, const double* src,
+                   double src_scale, void* stream);
+int fde_slab_diagonal(fde_slab h, double* d); /* host copy, (r1 - r0) * d1 values */
+int fde_slab_destroy(fde_slab h);
+/* out[c * rows + r] = in[r * cols + c] (row-major rows x cols -> cols x rows) */
+int fde_transpose(const double* in, double* out, size_t rows, size_t cols, void* stream);
+/* GridTransfer on row windows: `in` holds global rows starting at in_lo of its
+ * grid, `out` receives global rows [out_lo, out_lo + out_rows) of the other
+ * grid.  op 0 prolong (add != 0: out += P in), 1 restrict_full, 2 restrict_transpose. */
+int fde_transfer_rows(size_t n1, size_t n2, int coarsen_x, int coarsen_y, int op, int add,
+                      const double* in, size_t in_lo, double* out, size_t out_lo,
+                      size_t out_rows, void* stream);
+/* vector kernels: op 0 out = a * x .* y (zero-guess smoothing), 1 out += a * x
+ * (axpy, y unused), 2 out += a * x .* y (Jacobi update), 3 out = x * a (scale) */
+int fde_vec(int op, size_t n, double a, const double* x, const double* y, double* out,
+            void* stream);
+/* All-to-all layout helper.  Row ranges of the P ranks: offsets[0..P]
+ * (offsets[0] = 0, offsets[P] = d2).  dir 0 (unpack): in holds P chunks, chunk
+ * s = [nc][offsets[s+1]-offsets[s]] at element offset nc*offsets[s]; out is
+ * [nc][d2] with out[c*d2 + j] = chunk_owner(j)[c][j - offsets[owner]].  dir 1
+ * (pack) is the inverse map. */
+int fde_block_permute(const double* in, double* out, size_t nc, size_t d2,
+                      const long long* offsets_host, int nranks, int dir, void* stream);
+/* out += sgn * (*a_dev) * x (device scalar, e.g. a projection coefficient) */
+int fde_axpy_dev(size_t n, const double* a_dev, double sgn, const double* x, double* out,
+                 void* stream);
+/* *out_dev = <x, y> (deterministic two-level reduction; sqrt_out: sqrt of it) */
+int fde_dot(size_t n, const double* x, const double* y, double* out_dev, int sqrt_out,
+            void* stream);
+
 /* Number of kernels this library has launched since load (instrumentation). */
 unsigned long long fde_kernel_launches(void);
 

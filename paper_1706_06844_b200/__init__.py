@@ -129,6 +129,20 @@ _SIGS = {
     "fde_march_destroy": (_c_int, [_c_vp]),
     "fde_time_march": (_c_int, [ctypes.POINTER(_FdeProblem), _c_size, _c_size, _c_size,
                                 ctypes.POINTER(_DriverConfig), _P, ctypes.POINTER(_c_size), _P, _P]),
+    "fde_slab_create": (_c_int, [ctypes.POINTER(_FdeProblem)] + [_c_size] * 10 + [ctypes.POINTER(_c_vp)]),
+    "fde_slab_ypass": (_c_int, [_c_vp, _c_vp, _c_vp, _c_dbl, _c_vp]),
+    "fde_slab_xpass": (_c_int, [_c_vp, _c_vp, _c_vp, _c_vp, _c_dbl, _c_int, _c_vp, _c_vp, _c_dbl,
+                                _c_vp, _c_dbl, _c_vp]),
+    "fde_slab_diagonal": (_c_int, [_c_vp, _P]),
+    "fde_slab_destroy": (_c_int, [_c_vp]),
+    "fde_transpose": (_c_int, [_c_vp, _c_vp, _c_size, _c_size, _c_vp]),
+    "fde_transfer_rows": (_c_int, [_c_size, _c_size, _c_int, _c_int, _c_int, _c_int, _c_vp, _c_size,
+                                   _c_vp, _c_size, _c_size, _c_vp]),
+    "fde_vec": (_c_int, [_c_int, _c_size, _c_dbl, _c_vp, _c_vp, _c_vp, _c_vp]),
+    "fde_block_permute": (_c_int, [_c_vp, _c_vp, _c_size, _c_size, ctypes.POINTER(ctypes.c_longlong),
+                                   _c_int, _c_int, _c_vp]),
+    "fde_axpy_dev": (_c_int, [_c_size, _c_vp, _c_dbl, _c_vp, _c_vp, _c_vp]),
+    "fde_dot": (_c_int, [_c_size, _c_vp, _c_vp, _c_vp, _c_int, _c_vp]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGS)
 

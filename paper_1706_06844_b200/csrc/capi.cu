@@ -8,6 +8,7 @@
 #include "../../include/fde_b200.h"
 #include "krylov.cuh"
 #include "problem.cuh"
+#include "slab.cuh"
 
 namespace fde_b200 {
 std::atomic<unsigned long long> g_kernel_launches{0};
@@ -24,6 +25,9 @@ struct fde_mg_s {
 };
 struct fde_precond_s {
   std::shared_ptr<Precond> pc;
+};
+struct fde_slab_s {
+  std::unique_ptr<SlabOp> op;
 };
 struct fde_march_s {
   Problem p;
@@ -573,6 +577,116 @@ int fde_time_march(const fde_problem* p, size_t n1, size_t n2, size_t steps,
     *wall_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return rc != FDE_OK ? rc : rc2;
+}
+
+int fde_slab_create(const fde_problem* p, size_t nf1, size_t nf2, size_t d1, size_t d2,
+                    size_t steps, size_t m, size_t r0, size_t r1, size_t c0, size_t c1,
+                    fde_slab* out) {
+  return guard([&] {
+    need(out != nullptr, "null output");
+    auto h = std::make_unique<fde_slab_s>();
+    h->op = std::make_unique<SlabOp>(to_problem(p), nf1, nf2, d1, d2, steps, m, r0, r1, c0, c1);
+    *out = h.release();
+  });
+}
+int fde_slab_ypass(fde_slab h, const double* xT, double* QT, double sign, void* stream) {
+  return guard([&] {
+    need(h && xT && QT, "null argument");
+    h->op->ypass(xT, QT, sign, stream_of(stream));
+  });
+}
+int fde_slab_xpass(fde_slab h, const double* x, const double* Q, double* out, double sign,
+                   int epi, const double* b, const double* dinv, double omega, const double* src,
+                   double src_scale, void* stream) {
+  return guard([&] {
+    need(h && x && Q && out, "null argument");
+    need(epi >= EPI_STORE && epi <= EPI_JACOBI, "unknown epilogue");
+    need(epi != EPI_RHS || src, "rhs epilogue needs src");
+    need((epi != EPI_RESID && epi != EPI_JACOBI) || b, "epilogue needs b");
+    need(epi != EPI_JACOBI || dinv, "jacobi epilogue needs dinv");
+    EpiArgs e;
+    e.b = b;
+    e.dinv = dinv;
+    e.omega = omega;
+    e.src = src;
+    e.src_scale = src_scale;
+    h->op->xpass(x, Q, out, sign, epi, e, stream_of(stream));
+  });
+}
+int fde_slab_diagonal(fde_slab h, double* d) {
+  return guard([&] {
+    need(h && d, "null argument");
+    const auto& v = h->op->diagonal();
+    std::memcpy(d, v.data(), v.size() * sizeof(double));
+  });
+}
+int fde_slab_destroy(fde_slab h) {
+  return guard([&] { delete h; });
+}
+int fde_transpose(const double* in, double* out, size_t rows, size_t cols, void* stream) {
+  return guard([&] {
+    need(in && out && in != out, "transpose needs distinct buffers");
+    if (rows && cols) launch_transpose(in, out, (int)cols, (int)rows, stream_of(stream));
+  });
+}
+int fde_transfer_rows(size_t n1, size_t n2, int coarsen_x, int coarsen_y, int op, int add,
+                      const double* in, size_t in_lo, double* out, size_t out_lo,
+                      size_t out_rows, void* stream) {
+  return guard([&] {
+    need(in && out, "null argument");
+    const Xfer t = make_xfer((int)n1, (int)n2, coarsen_x != 0, coarsen_y != 0);
+    if (op == 0) {
+      need(out_lo + out_rows <= n2, "fine row window out of range");
+      xfer_prolong_rows(t, in, (int)in_lo, out, (int)out_lo, (int)out_rows, add != 0,
+                        stream_of(stream));
+    } else if (op == 1 || op == 2) {
+      need(out_lo + out_rows <= (size_t)t.k2, "coarse row window out of range");
+      xfer_restrict_rows(t, in, (int)in_lo, out, (int)out_lo, (int)out_rows, op == 1 ? 0.5 : 1.0,
+                         stream_of(stream));
+    } else {
+      throw InvalidArgument("transfer op must be 0, 1 or 2");
+    }
+  });
+}
+int fde_vec(int op, size_t n, double a, const double* x, const double* y, double* out,
+            void* stream) {
+  return guard([&] {
+    need(x && out, "null argument");
+    cudaStream_t s = stream_of(stream);
+    switch (op) {
+      case 0: need(y != nullptr, "null y"); vec_diag_scale(n, a, x, y, out, s); break;
+      case 1: vec_axpy(n, a, x, out, s); break;
+      case 2: need(y != nullptr, "null y"); vec_jacobi_update(n, a, x, y, out, s); break;
+      case 3: vec_copy_scale(n, a, x, out, s); break;
+      default: throw InvalidArgument("unknown vector op");
+    }
+  });
+}
+int fde_block_permute(const double* in, double* out, size_t nc, size_t d2,
+                      const long long* offsets_host, int nranks, int dir, void* stream) {
+  return guard([&] {
+    need(in && out && offsets_host && nranks > 0 && nranks <= 64, "bad block permute arguments");
+    need(offsets_host[0] == 0 && (size_t)offsets_host[nranks] == d2, "offsets must span [0, d2]");
+    long long off[65];
+    for (int r = 0; r <= nranks; ++r) off[r] = offsets_host[r];
+    block_permute(in, out, nc, d2, off, nranks, dir, stream_of(stream));
+  });
+}
+int fde_axpy_dev(size_t n, const double* a_dev, double sgn, const double* x, double* out,
+                 void* stream) {
+  return guard([&] {
+    need(a_dev && x && out, "null argument");
+    vec_axpy_dev(n, a_dev, sgn, x, out, stream_of(stream));
+  });
+}
+int fde_dot(size_t n, const double* x, const double* y, double* out_dev, int sqrt_out,
+            void* stream) {
+  return guard([&] {
+    need(x && y && out_dev, "null argument");
+    static thread_local std::unique_ptr<Reducer> red;
+    if (!red) red = std::make_unique<Reducer>();
+    red->dot(n, x, y, out_dev, stream_of(stream), sqrt_out != 0);
+  });
 }
 
 }  // extern "C"

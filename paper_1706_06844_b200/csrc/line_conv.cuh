@@ -64,7 +64,8 @@ struct YPass {
   const double* epT;  // ep transposed: epT[i * n2 + j] = ep[i + j * n1]
   const double* emT;
   double c;           // sign * s_over_r
-  double* q;          // Q[i + j * n1]
+  double* q;          // Q[i + j * n1], or Q transposed (Q[i * n2 + j]) when qT is set
+  int qT;
   __device__ __forceinline__ int nlines() const { return n1; }
   __device__ __forceinline__ double load(int line, int pos) const {
     return xT ? x[(size_t)line * n2 + pos] : x[(size_t)pos * n1 + line];
@@ -75,7 +76,9 @@ struct YPass {
   }
   __device__ __forceinline__ void finish(int line, int pos, double ty, double tt,
                                          const Ops& o) const {
-    q[(size_t)pos * n1 + line] = c * (o.ep * ty + o.em * tt);
+    const double v = c * (o.ep * ty + o.em * tt);
+    if (qT) q[(size_t)line * n2 + pos] = v;
+    else q[(size_t)pos * n1 + line] = v;
   }
 };
 

@@ -31,6 +31,14 @@ __global__ void k_scale_inv_dev(size_t n, const double* __restrict__ a, const do
   const double inv = 1.0 / *a;
   GRID_STRIDE(i, n) y[i] = x[i] * inv;
 }
+__global__ void k_jacobi_upd(size_t n, double a, const double* __restrict__ d,
+                             const double* __restrict__ r, double* __restrict__ x) {
+  GRID_STRIDE(i, n) x[i] += a * d[i] * r[i];
+}
+__global__ void k_copy_scale2(size_t n, double a, const double* __restrict__ x,
+                              double* __restrict__ y) {
+  GRID_STRIDE(i, n) y[i] = x[i] * a;
+}
 __global__ void k_scal(size_t n, double a, double* x) {
   GRID_STRIDE(i, n) x[i] *= a;
 }
@@ -177,25 +185,29 @@ __device__ __forceinline__ double rrow(const double* f, int n, int fc, double sc
   return sc * v;
 }
 
-__global__ void k_restrict(Xfer t, const double* __restrict__ f, double* __restrict__ c,
-                           double sc) {
-  const size_t nc = (size_t)t.k1 * t.k2;
+// Row windows let the same kernels run on a y-slab: the fine buffer holds
+// global fine rows [f_lo, f_lo + rows), the coarse buffer global coarse rows
+// [c_lo, c_lo + rows).  Full-grid calls use f_lo = c_lo = 0.
+__global__ void k_restrict(Xfer t, const double* __restrict__ f, int f_lo,
+                           double* __restrict__ c, int c_lo, int c_rows, double sc) {
+  const size_t nc = (size_t)t.k1 * c_rows;
   GRID_STRIDE(q, nc) {
-    const int a = (int)(q % t.k1), bb = (int)(q / t.k1);
+    const int a = (int)(q % t.k1), bb = (int)(q / t.k1) + c_lo;  // global coarse row
+    auto frow = [&](int r) { return f + (size_t)(r - f_lo) * t.n1; };
     double out;
     if (!t.cx) {  // restrict_cols only (multigrid.cpp:60-71)
       const int fb = 2 * bb + 1 - t.par2;
-      double v = f[(size_t)fb * t.n1 + a];
-      if (fb > 0) v += 0.5 * f[(size_t)(fb - 1) * t.n1 + a];
-      if (fb + 1 < t.n2) v += 0.5 * f[(size_t)(fb + 1) * t.n1 + a];
+      double v = frow(fb)[a];
+      if (fb > 0) v += 0.5 * frow(fb - 1)[a];
+      if (fb + 1 < t.n2) v += 0.5 * frow(fb + 1)[a];
       out = v * sc;
     } else if (!t.cy) {  // restrict_rows only
-      out = rrow(f + (size_t)bb * t.n1, t.n1, 2 * a + 1 - t.par1, sc);
+      out = rrow(frow(bb), t.n1, 2 * a + 1 - t.par1, sc);
     } else {  // rows then columns of the row-restricted temporary
       const int fa = 2 * a + 1 - t.par1, fb = 2 * bb + 1 - t.par2;
-      double v = rrow(f + (size_t)fb * t.n1, t.n1, fa, sc);
-      if (fb > 0) v += 0.5 * rrow(f + (size_t)(fb - 1) * t.n1, t.n1, fa, sc);
-      if (fb + 1 < t.n2) v += 0.5 * rrow(f + (size_t)(fb + 1) * t.n1, t.n1, fa, sc);
+      double v = rrow(frow(fb), t.n1, fa, sc);
+      if (fb > 0) v += 0.5 * rrow(frow(fb - 1), t.n1, fa, sc);
+      if (fb + 1 < t.n2) v += 0.5 * rrow(frow(fb + 1), t.n1, fa, sc);
       out = v * sc;
     }
     c[q] = out;
@@ -219,38 +231,58 @@ __device__ __forceinline__ double prow(const double* c, int k, int i, int par) {
 }
 
 template <bool ADD>
-__global__ void k_prolong(Xfer t, const double* __restrict__ c, double* __restrict__ f) {
-  const size_t nf = (size_t)t.n1 * t.n2;
+__global__ void k_prolong(Xfer t, const double* __restrict__ c, int c_lo,
+                          double* __restrict__ f, int f_lo, int f_rows) {
+  const size_t nf = (size_t)t.n1 * f_rows;
   GRID_STRIDE(q, nf) {
-    const int i = (int)(q % t.n1), j = (int)(q / t.n1);
+    const int i = (int)(q % t.n1), j = (int)(q / t.n1) + f_lo;  // global fine row
+    auto crow = [&](int r, int width) { return c + (size_t)(r - c_lo) * width; };
     double v;
     if (!t.cx) {  // prolong_cols only: rows of width n1 (multigrid.cpp:34-44)
       const int tt = j - 1 + t.par2;
       if ((tt & 1) == 0) {
         const int jc = tt >> 1;
-        v = (jc >= 0 && jc < t.k2) ? c[(size_t)jc * t.n1 + i] : 0.0;
+        v = (jc >= 0 && jc < t.k2) ? crow(jc, t.n1)[i] : 0.0;
       } else {
         const int jl = (tt - 1) >> 1, jr = jl + 1;
         v = 0.0;
-        if (jl >= 0 && jl < t.k2) v += 0.5 * c[(size_t)jl * t.n1 + i];
-        if (jr >= 0 && jr < t.k2) v += 0.5 * c[(size_t)jr * t.n1 + i];
+        if (jl >= 0 && jl < t.k2) v += 0.5 * crow(jl, t.n1)[i];
+        if (jr >= 0 && jr < t.k2) v += 0.5 * crow(jr, t.n1)[i];
       }
     } else if (!t.cy) {  // prolong_rows only
-      v = prow(c + (size_t)j * t.k1, t.k1, i, t.par1);
+      v = prow(crow(j, t.k1), t.k1, i, t.par1);
     } else {  // rows into tmp (n1 x k2), then columns
       const int tt = j - 1 + t.par2;
       if ((tt & 1) == 0) {
         const int jc = tt >> 1;
-        v = (jc >= 0 && jc < t.k2) ? prow(c + (size_t)jc * t.k1, t.k1, i, t.par1) : 0.0;
+        v = (jc >= 0 && jc < t.k2) ? prow(crow(jc, t.k1), t.k1, i, t.par1) : 0.0;
       } else {
         const int jl = (tt - 1) >> 1, jr = jl + 1;
         v = 0.0;
-        if (jl >= 0 && jl < t.k2) v += 0.5 * prow(c + (size_t)jl * t.k1, t.k1, i, t.par1);
-        if (jr >= 0 && jr < t.k2) v += 0.5 * prow(c + (size_t)jr * t.k1, t.k1, i, t.par1);
+        if (jl >= 0 && jl < t.k2) v += 0.5 * prow(crow(jl, t.k1), t.k1, i, t.par1);
+        if (jr >= 0 && jr < t.k2) v += 0.5 * prow(crow(jr, t.k1), t.k1, i, t.par1);
       }
     }
     if (ADD) f[q] += v;
     else f[q] = v;
+  }
+}
+
+struct RankOffsets {
+  long long o[65];
+  int n;
+};
+__global__ void k_block_permute(const double* __restrict__ in, double* __restrict__ out,
+                                size_t nc, size_t d2, RankOffsets ro, int dir) {
+  const size_t total = nc * d2;
+  GRID_STRIDE(q, total) {
+    const size_t c = q / d2, j = q % d2;
+    int s = 0;
+    while (s + 1 < ro.n && (long long)j >= ro.o[s + 1]) ++s;
+    const size_t rows = (size_t)(ro.o[s + 1] - ro.o[s]);
+    const size_t src = nc * (size_t)ro.o[s] + c * rows + (j - (size_t)ro.o[s]);
+    if (dir == 0) out[q] = in[src];
+    else out[src] = in[q];
   }
 }
 
@@ -299,6 +331,15 @@ void vec_scal(size_t n, double a, double* x, cudaStream_t s) {
   k_scal<<<blocks_for(n), kThreads, 0, s>>>(n, a, x);
   FDE_LAUNCH_CHECK();
 }
+void vec_jacobi_update(size_t n, double a, const double* d, const double* r, double* out,
+                       cudaStream_t s) {
+  k_jacobi_upd<<<blocks_for(n), kThreads, 0, s>>>(n, a, d, r, out);
+  FDE_LAUNCH_CHECK();
+}
+void vec_copy_scale(size_t n, double a, const double* x, double* y, cudaStream_t s) {
+  k_copy_scale2<<<blocks_for(n), kThreads, 0, s>>>(n, a, x, y);
+  FDE_LAUNCH_CHECK();
+}
 void vec_sub(size_t n, const double* x, const double* y, double* out, cudaStream_t s) {
   k_sub<<<blocks_for(n), kThreads, 0, s>>>(n, x, y, out);
   FDE_LAUNCH_CHECK();
@@ -345,20 +386,39 @@ Xfer make_xfer(int n1, int n2, bool cx, bool cy) {
   if (t.k1 == 0 || t.k2 == 0 || (!cx && !cy)) throw InvalidArgument("grid too small to coarsen");
   return t;
 }
+void xfer_restrict_rows(const Xfer& t, const double* fine, int f_lo, double* coarse, int c_lo,
+                        int c_rows, double scale, cudaStream_t s) {
+  const size_t nc = (size_t)t.k1 * c_rows;
+  if (!nc) return;
+  k_restrict<<<blocks_for(nc), kThreads, 0, s>>>(t, fine, f_lo, coarse, c_lo, c_rows, scale);
+  FDE_LAUNCH_CHECK();
+}
+void xfer_prolong_rows(const Xfer& t, const double* coarse, int c_lo, double* fine, int f_lo,
+                       int f_rows, bool add, cudaStream_t s) {
+  const size_t nf = (size_t)t.n1 * f_rows;
+  if (!nf) return;
+  if (add) k_prolong<true><<<blocks_for(nf), kThreads, 0, s>>>(t, coarse, c_lo, fine, f_lo, f_rows);
+  else k_prolong<false><<<blocks_for(nf), kThreads, 0, s>>>(t, coarse, c_lo, fine, f_lo, f_rows);
+  FDE_LAUNCH_CHECK();
+}
 void xfer_restrict(const Xfer& t, const double* fine, double* coarse, double scale,
                    cudaStream_t s) {
-  const size_t nc = (size_t)t.k1 * t.k2;
-  k_restrict<<<blocks_for(nc), kThreads, 0, s>>>(t, fine, coarse, scale);
-  FDE_LAUNCH_CHECK();
+  xfer_restrict_rows(t, fine, 0, coarse, 0, t.k2, scale, s);
 }
 void xfer_prolong_add(const Xfer& t, const double* coarse, double* fine, cudaStream_t s) {
-  const size_t nf = (size_t)t.n1 * t.n2;
-  k_prolong<true><<<blocks_for(nf), kThreads, 0, s>>>(t, coarse, fine);
-  FDE_LAUNCH_CHECK();
+  xfer_prolong_rows(t, coarse, 0, fine, 0, t.n2, true, s);
 }
 void xfer_prolong(const Xfer& t, const double* coarse, double* fine, cudaStream_t s) {
-  const size_t nf = (size_t)t.n1 * t.n2;
-  k_prolong<false><<<blocks_for(nf), kThreads, 0, s>>>(t, coarse, fine);
+  xfer_prolong_rows(t, coarse, 0, fine, 0, t.n2, false, s);
+}
+void block_permute(const double* in, double* out, size_t nc, size_t d2, const long long* off,
+                   int nranks, int dir, cudaStream_t s) {
+  RankOffsets ro{};
+  for (int r = 0; r <= nranks; ++r) ro.o[r] = off[r];
+  ro.n = nranks;
+  const size_t total = nc * d2;
+  if (!total) return;
+  k_block_permute<<<blocks_for(total), kThreads, 0, s>>>(in, out, nc, d2, ro, dir);
   FDE_LAUNCH_CHECK();
 }
 void lu_solve(int n, const double* lu, const int* perm, const double* b, double* x,

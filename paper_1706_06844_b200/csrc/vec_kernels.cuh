@@ -20,6 +20,11 @@ void vec_scale_inv_dev(size_t n, const double* a_dev, const double* x, double* y
                        cudaStream_t s);
 // x *= a
 void vec_scal(size_t n, double a, double* x, cudaStream_t s);
+// out += a * d .* r   (Jacobi update, multigrid.cpp:380-382)
+void vec_jacobi_update(size_t n, double a, const double* d, const double* r, double* out,
+                       cudaStream_t s);
+// y = x * a
+void vec_copy_scale(size_t n, double a, const double* x, double* y, cudaStream_t s);
 // out = x - y
 void vec_sub(size_t n, const double* x, const double* y, double* out, cudaStream_t s);
 // out = x0 + sum_k c[k] * v[k]   accumulated in k order (krylov.cpp:136-137,153-155)
@@ -59,6 +64,18 @@ void xfer_restrict(const Xfer& t, const double* fine, double* coarse, double sca
 void xfer_prolong_add(const Xfer& t, const double* coarse, double* fine, cudaStream_t s);
 // fine = P coarse
 void xfer_prolong(const Xfer& t, const double* coarse, double* fine, cudaStream_t s);
+// Row-window variants for y-slabs: the fine buffer holds global fine rows
+// starting at f_lo, the coarse buffer global coarse rows starting at c_lo.
+// restrict writes coarse rows [c_lo, c_lo + c_rows); prolong writes fine
+// rows [f_lo, f_lo + f_rows) (add: +=).  Needed neighbour rows must be present.
+void xfer_restrict_rows(const Xfer& t, const double* fine, int f_lo, double* coarse, int c_lo,
+                        int c_rows, double scale, cudaStream_t s);
+void xfer_prolong_rows(const Xfer& t, const double* coarse, int c_lo, double* fine, int f_lo,
+                       int f_rows, bool add, cudaStream_t s);
+
+// All-to-all chunk layout <-> [nc][d2] (see fde_block_permute); off[0..P].
+void block_permute(const double* in, double* out, size_t nc, size_t d2, const long long* off,
+                   int nranks, int dir, cudaStream_t s);
 
 // x = U^-1 L^-1 P b on one CTA (coarsest CoarseSolve::lu, multigrid.cpp:324-328).
 void lu_solve(int n, const double* lu, const int* perm, const double* b, double* x,

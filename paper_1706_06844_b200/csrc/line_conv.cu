@@ -258,6 +258,9 @@ struct Fft {
 #ifndef FDE_PTS
 #define FDE_PTS 16
 #endif
+#ifndef FDE_L2_PREFETCH
+#define FDE_L2_PREFETCH 1
+#endif
 #ifndef FDE_MINB_BIG
 #define FDE_MINB_BIG 2
 #endif
@@ -291,6 +294,12 @@ __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
   const int n = p.blk.n;
   double* const ra = smem + (size_t)ls * 2 * BUF;
   double* const ia = ra + BUF;
+
+  // 0) warm L2 with the epilogue operands of this line (consumed ~3 FFTs later)
+#if FDE_L2_PREFETCH
+  if (active)
+    for (int c = tl; c * 16 < n; c += T) p.prefetch(line, c);
+#endif
 
   // 1) z_m = x_2m + i x_2m+1, m = tl + s*T; zero padded (n <= M: s < P/2 only)
   double2 v[P];

@@ -40,6 +40,10 @@ struct LineBlockDev {
   const double* row;     // first row, n entries (direct path)
 };
 
+__device__ __forceinline__ void l2_prefetch(const double* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 enum Epilogue : int {
   EPI_STORE = 0,   // out = A x                       (LinOp::apply)
   EPI_RHS = 1,     // out = A~ x + src_scale * src     (assemble_rhs, problem.cpp:73-89)
@@ -74,6 +78,14 @@ struct YPass {
     const size_t t = (size_t)line * n2 + pos;
     return Ops{epT[t], emT[t]};
   }
+  // warm L2 with this line's epilogue operands (one 128-byte line per call)
+  __device__ __forceinline__ void prefetch(int line, int chunk) const {
+    const size_t t = (size_t)line * n2 + (size_t)chunk * 16;
+    if ((size_t)chunk * 16 < (size_t)n2) {
+      l2_prefetch(epT + t);
+      l2_prefetch(emT + t);
+    }
+  }
   __device__ __forceinline__ void finish(int line, int pos, double ty, double tt,
                                          const Ops& o) const {
     const double v = c * (o.ep * ty + o.em * tt);
@@ -107,6 +119,17 @@ struct XPass {
   __device__ __forceinline__ int nlines() const { return n2; }
   __device__ __forceinline__ double load(int line, int pos) const {
     return x[(size_t)line * n1 + pos];
+  }
+  __device__ __forceinline__ void prefetch(int line, int chunk) const {
+    const size_t p = (size_t)line * n1 + (size_t)chunk * 16;
+    if ((size_t)chunk * 16 < (size_t)n1) {
+      l2_prefetch(dp + p);
+      l2_prefetch(dm + p);
+      if (q) l2_prefetch(q + p);
+      if (epi == EPI_RHS) l2_prefetch(src + p);
+      if (epi == EPI_RESID || epi == EPI_JACOBI) l2_prefetch(b + p);
+      if (epi == EPI_JACOBI) l2_prefetch(dinv + p);
+    }
   }
   __device__ __forceinline__ Ops fetch(int line, int pos) const {
     const size_t p = (size_t)line * n1 + pos;

@@ -288,8 +288,9 @@ __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
   using S = FftShape<LOGM>;
   constexpr int M = S::M, T = S::T, BUF = S::BUF, P = S::P, H = P / 2, SH = Log2<P>::v;
   extern __shared__ double smem[];
+  // lines per CTA is a launch-time choice (<= S::LPB): small levels use more CTAs
   const int ls = threadIdx.x / T, tl = threadIdx.x - ls * T;
-  const int line = blockIdx.x * S::LPB + ls;
+  const int line = blockIdx.x * (int)(blockDim.x / T) + ls;
   const bool active = line < p.nlines();
   const int n = p.blk.n;
   double* const ra = smem + (size_t)ls * 2 * BUF;
@@ -388,28 +389,53 @@ __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
   }
 }
 
-// Warp-per-line direct Toeplitz product for short lines (n <= 32).
+// Warp-per-line direct Toeplitz product for short lines (n <= kDirectMax):
+// up to four outputs per lane, x broadcast by shuffles, the block's first
+// column / row staged in shared memory.  Exact sums, no FFT latency chain --
+// this is what the coarse multigrid levels run.
 template <class P>
 __global__ void __launch_bounds__(256) direct_line_kernel(const P p) {
+  constexpr int E = kDirectMax / 32;
+  __shared__ double s_col[kDirectMax], s_row[kDirectMax];
+  const int n = p.blk.n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    s_col[i] = p.blk.col[i];
+    s_row[i] = p.blk.row[i];
+  }
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int line = blockIdx.x * 8 + warp;
   if (line >= p.nlines()) return;
-  const int n = p.blk.n;
-  const double xv = lane < n ? p.load(line, lane) : 0.0;
-  double ty = 0.0, tt = 0.0;
-  const double* __restrict__ col = p.blk.col;
-  const double* __restrict__ row = p.blk.row;
-  for (int k = 0; k < n; ++k) {
-    const double xk = __shfl_sync(0xffffffffu, xv, k);
-    if (lane < n) {
-      const double a = lane >= k ? __ldg(&col[lane - k]) : __ldg(&row[k - lane]);  // T(i,k)
-      const double b = k >= lane ? __ldg(&col[k - lane]) : __ldg(&row[lane - k]);  // T(k,i)
-      ty += a * xk;
-      tt += b * xk;
+  double xv[E], ty[E], tt[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = lane + 32 * e;
+    xv[e] = i < n ? p.load(line, i) : 0.0;
+    ty[e] = 0.0;
+    tt[e] = 0.0;
+  }
+#pragma unroll
+  for (int kb = 0; kb < E; ++kb) {
+    if (32 * kb >= n) break;
+    const int kend = n - 32 * kb < 32 ? n - 32 * kb : 32;
+    for (int kk = 0; kk < kend; ++kk) {
+      const int k = 32 * kb + kk;
+      const double xk = __shfl_sync(0xffffffffu, xv[kb], kk);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = lane + 32 * e;
+        if (i < n) {
+          ty[e] = fma(i >= k ? s_col[i - k] : s_row[k - i], xk, ty[e]);  // T(i,k)
+          tt[e] = fma(k >= i ? s_col[k - i] : s_row[i - k], xk, tt[e]);  // T(k,i)
+        }
+      }
     }
   }
-  if (lane < n) p.finish(line, lane, ty, tt, p.fetch(line, lane));
-  (void)xv;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = lane + 32 * e;
+    if (i < n) p.finish(line, i, ty[e], tt[e], p.fetch(line, i));
+  }
 }
 
 // 32 x 32 tiles, 32 x 8 threads; padded shared tile (8-byte banks).
@@ -445,8 +471,21 @@ void launch_fft(const P& p, cudaStream_t s) {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
     configured = true;
   }
-  const int grid = (lines_of(p) + S::LPB - 1) / S::LPB;
-  fft_line_kernel<LOGM, P><<<grid, S::THREADS, S::SMEM, s>>>(p);
+  // spread small levels over the SMs: fewer lines per CTA until the grid
+  // covers two waves (CTAs stay a whole number of warps)
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    FDE_CUDA(cudaGetDevice(&dev));
+    FDE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int lines = lines_of(p);
+  int lpb = S::LPB;
+  const int min_lpb = S::T >= 32 ? 1 : 32 / S::T;
+  while (lpb > min_lpb && (lines + lpb - 1) / lpb < 2 * sms) lpb /= 2;
+  const int grid = (lines + lpb - 1) / lpb;
+  const size_t smem = size_t(lpb) * 2 * S::BUF * sizeof(double);
+  fft_line_kernel<LOGM, P><<<grid, S::T * lpb, smem, s>>>(p);
   FDE_LAUNCH_CHECK();
 }
 

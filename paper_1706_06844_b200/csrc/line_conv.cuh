@@ -21,8 +21,8 @@
 //    ep/em; the x-pass (rows, contiguous) adds inv_r x + sign (dp T_a x +
 //    dm T_a^T x) + Q and applies a fused epilogue (plain store, rhs source
 //    add, residual b - Ax, damped-Jacobi update) -- all its streams coalesced.
-//  * Lines with n <= kDirectMax use a warp-per-line direct product (coarse
-//    multigrid levels, semicoarsened n = 1 lines).
+//  * Lines with n <= kDirectMax (32) use a warp-per-line direct product
+//    (coarse multigrid levels, semicoarsened n = 1 lines).
 #pragma once
 #include "common.cuh"
 

@@ -457,6 +457,32 @@ __global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict
   }
 }
 
+// Same tiling with the input map applied on the way in; the mapped values are
+// also stored row-major when xout is set (read and written by the same thread).
+template <int K>
+__global__ void __launch_bounds__(256) transpose_map_kernel(const InMap m, double* xout,
+                                                            double* __restrict__ out, int n1,
+                                                            int n2) {
+  __shared__ double tile[32][33];
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    const int i = i0 + tx, j = j0 + ty + k;
+    if (i < n1 && j < n2) {
+      const double v = m.at<K>(i, j);
+      tile[ty + k][tx] = v;
+      if (xout) xout[(size_t)j * n1 + i] = v;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    const int j = j0 + tx, i = i0 + ty + k;
+    if (i < n1 && j < n2) out[(size_t)i * n2 + j] = tile[tx][ty + k];
+  }
+}
+
 template <class P>
 int lines_of(const P& p) {
   return std::is_same<P, YPass>::value ? p.n1 : p.n2;
@@ -515,6 +541,17 @@ void launch_line_pass(const YPass& p, cudaStream_t s) { launch_any(p, s); }
 void launch_transpose(const double* in, double* out, int n1, int n2, cudaStream_t s) {
   const dim3 grid((n1 + 31) / 32, (n2 + 31) / 32);
   transpose_kernel<<<grid, 256, 0, s>>>(in, out, n1, n2);
+  FDE_LAUNCH_CHECK();
+}
+void launch_transpose_mapped(const InMap& m, double* xout, double* out, int n1, int n2,
+                             cudaStream_t s) {
+  const dim3 grid((n1 + 31) / 32, (n2 + 31) / 32);
+  switch (m.kind) {
+    case 0: transpose_map_kernel<0><<<grid, 256, 0, s>>>(m, xout, out, n1, n2); break;
+    case 1: transpose_map_kernel<1><<<grid, 256, 0, s>>>(m, xout, out, n1, n2); break;
+    case 2: transpose_map_kernel<2><<<grid, 256, 0, s>>>(m, xout, out, n1, n2); break;
+    default: throw InvalidArgument("unknown operator input map");
+  }
   FDE_LAUNCH_CHECK();
 }
 void launch_line_pass(const XPass& p, cudaStream_t s) { launch_any(p, s); }

@@ -25,6 +25,7 @@
 //    (coarse multigrid levels, semicoarsened n = 1 lines).
 #pragma once
 #include "common.cuh"
+#include "transfer.cuh"
 
 namespace fde_b200 {
 
@@ -43,6 +44,28 @@ struct LineBlockDev {
 __device__ __forceinline__ void l2_prefetch(const double* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
+
+// Operator input evaluated by the column-transpose pass, so a multigrid
+// update folds into the next operator application instead of its own pass:
+//   kind 0: a                       (plain)
+//   kind 1: (w * d) * a              zero-guess smoothing x = omega dinv b (multigrid.cpp:355-356)
+//   kind 2: a + (P c)                prolongation correction x + P xc (multigrid.cpp:377-378)
+struct InMap {
+  int kind;
+  const double* a;
+  const double* d;
+  double w;
+  Xfer t;
+  const double* c;
+  int ld;  // row length of a / d
+  template <int K>
+  __device__ __forceinline__ double at(int i, int j) const {
+    const size_t p = (size_t)j * ld + i;
+    if constexpr (K == 1) return w * d[p] * a[p];
+    else if constexpr (K == 2) return a[p] + prolong_point(t, c, 0, i, j);
+    else return a[p];
+  }
+};
 
 enum Epilogue : int {
   EPI_STORE = 0,   // out = A x                       (LinOp::apply)
@@ -166,6 +189,10 @@ struct XPass {
 void launch_line_pass(const YPass& p, cudaStream_t s);
 // out[i * n2 + j] = in[i + j * n1] (tiled through shared memory)
 void launch_transpose(const double* in, double* out, int n1, int n2, cudaStream_t s);
+// out[i * n2 + j] = v(i, j) = m.at(i, j), and xout[i + j * n1] = v(i, j) when
+// xout is set (it may alias m.a: each element is read and written by one thread)
+void launch_transpose_mapped(const InMap& m, double* xout, double* out, int n1, int n2,
+                             cudaStream_t s);
 void launch_line_pass(const XPass& p, cudaStream_t s);
 
 }  // namespace fde_b200

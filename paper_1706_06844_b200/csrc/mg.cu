@@ -1,5 +1,6 @@
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 
 #include "mg.cuh"
 
@@ -139,6 +140,9 @@ Hierarchy::Hierarchy(std::vector<LevelOp> levels, std::vector<std::pair<size_t, 
     : levels_(std::move(levels)), dims_(std::move(dims)), mode_(mode), omega_(omega),
       coarse_(coarse), coarse_sweeps_(coarse_sweeps) {
   if (levels_.empty()) throw InvalidArgument("empty hierarchy");
+  // bit 0: fold zero-guess smoothing into the residual pass, bit 1: fold the
+  // prolongation correction into the post-smoothing pass (both bit-identical)
+  if (const char* e = std::getenv("FDE_MG_FUSE")) fuse_ = std::atoi(e);
   if (levels_.size() != dims_.size()) throw InvalidArgument("level dims mismatch");
   if (!(omega_ > 0.0)) throw InvalidArgument("omega must be positive");
   if (coarse_ == COARSE_SWEEPS && coarse_sweeps_ == 0)
@@ -207,26 +211,57 @@ void Hierarchy::cycle(size_t l, const double* b, double* x, bool zero, cudaStrea
       FDE_LAUNCH_CHECK();
     }
   };
+  // zero-guess smoothing x = omega dinv b (multigrid.cpp:355-356) and the
+  // correction x + P xc (multigrid.cpp:377-378) ride on the next operator
+  // application's column transpose where the level has one (fine levels)
+  const bool mapped = lev.sop && lev.sop->maps_input();
+  InMap zin{};
+  zin.kind = 1;
+  zin.a = b;
+  zin.d = dinv;
+  zin.w = omega_;
+  zin.ld = (int)dims_[l].first;
   if (l + 1 == levels_.size()) {  // multigrid.cpp:322-350
     if (coarse_ == COARSE_LU) {
       lu_solve((int)n, lu_.get(), perm_.get(), b, x, s);
     } else if (coarse_ == COARSE_SWEEPS) {
-      if (zero) vec_diag_scale(n, omega_, dinv, b, x, s);
-      else sweep();
-      for (size_t k = 1; k < coarse_sweeps_; ++k) sweep();
+      size_t k = 1;
+      if (!zero) {
+        sweep();
+      } else if (mapped && (fuse_ & 1) && coarse_sweeps_ > 1) {
+        lev.sop->run_mapped(zin, x, x, 1.0, EPI_JACOBI, jac, s);  // first two sweeps
+        k = 2;
+      } else {
+        vec_diag_scale(n, omega_, dinv, b, x, s);
+      }
+      for (; k < coarse_sweeps_; ++k) sweep();
     }
     return;
   }
-  if (zero) vec_diag_scale(n, omega_, dinv, b, x, s);  // multigrid.cpp:355-356
-  else sweep();
   EpiArgs res;
   res.b = b;
-  lev.run(x, r_[l].get(), EPI_RESID, res, s);  // r = b - A x
+  if (zero && mapped && (fuse_ & 1)) {
+    lev.sop->run_mapped(zin, x, r_[l].get(), 1.0, EPI_RESID, res, s);  // x, r = b - A x
+  } else {
+    if (zero) vec_diag_scale(n, omega_, dinv, b, x, s);
+    else sweep();
+    lev.run(x, r_[l].get(), EPI_RESID, res, s);  // r = b - A x
+  }
   xfer_restrict(xfer_[l], r_[l].get(), bc_[l + 1].get(), mode_ == MODE_GALERKIN ? 1.0 : 0.5, s);
   if (l + 2 == levels_.size() && coarse_ == COARSE_NONE) xc_[l + 1].zero(s);
   cycle(l + 1, bc_[l + 1].get(), xc_[l + 1].get(), true, s);
-  xfer_prolong_add(xfer_[l], xc_[l + 1].get(), x, s);  // x += P xc
-  sweep();                                              // post-smooth
+  if (mapped && (fuse_ & 2)) {
+    InMap pin{};
+    pin.kind = 2;
+    pin.a = x;
+    pin.t = xfer_[l];
+    pin.c = xc_[l + 1].get();
+    pin.ld = (int)dims_[l].first;
+    lev.sop->run_mapped(pin, x, x, 1.0, EPI_JACOBI, jac, s);  // x += P xc, post-smooth
+  } else {
+    xfer_prolong_add(xfer_[l], xc_[l + 1].get(), x, s);  // x += P xc
+    sweep();                                              // post-smooth
+  }
 }
 
 }  // namespace fde_b200

@@ -69,6 +69,7 @@ class Hierarchy {
   double omega_;
   int coarse_;
   size_t coarse_sweeps_;
+  int fuse_ = 3;
   DevBuf<double> lu_;
   DevBuf<int> perm_;
 };

@@ -221,15 +221,34 @@ void StructuredOp::scale(double s) {
   d_diag_.upload(diag_.data(), n);
 }
 
+bool StructuredOp::maps_input() const {
+  return ay_.dev().logM && n1_ >= 512 && transpose_columns_;
+}
+
 void StructuredOp::run(const double* x, double* out, double sign, int epi, const EpiArgs& e,
                        cudaStream_t s) const {
+  run_impl(nullptr, x, out, sign, epi, e, s);
+}
+
+void StructuredOp::run_mapped(const InMap& in, double* x, double* out, double sign, int epi,
+                              const EpiArgs& e, cudaStream_t s) const {
+  if (!maps_input()) throw InvalidArgument("operator input map needs the transposed column pass");
+  run_impl(&in, x, out, sign, epi, e, s);
+}
+
+void StructuredOp::run_impl(const InMap* in, const double* x, double* out, double sign, int epi,
+                            const EpiArgs& e, cudaStream_t s) const {
   YPass yp{};
   yp.blk = ay_.dev();
   yp.n1 = (int)n1_;
   yp.n2 = (int)n2_;
   yp.x = x;
   // FFT-path columns read a transposed copy (coalesced) instead of stride-n1 gathers
-  if (yp.blk.logM && n1_ >= 512 && transpose_columns_) {
+  if (in) {
+    launch_transpose_mapped(*in, const_cast<double*>(x), d_xT_.get(), (int)n1_, (int)n2_, s);
+    yp.x = d_xT_.get();
+    yp.xT = 1;
+  } else if (maps_input()) {
     launch_transpose(x, d_xT_.get(), (int)n1_, (int)n2_, s);
     yp.x = d_xT_.get();
     yp.xT = 1;

@@ -74,6 +74,13 @@ class StructuredOp {
   // EPI_JACOBI.  Not re-entrant across streams (one Q scratch per operator).
   void run(const double* x, double* out, double sign, int epi, const EpiArgs& e,
            cudaStream_t s) const;
+  // Whether run_mapped is available: the column pass reads a transposed copy
+  // of x, so the input map rides on that transpose.
+  bool maps_input() const;
+  // x = in(.) is formed (and stored to x, which may alias in.a) by the column
+  // transpose, then out = epi(A x) as in run().
+  void run_mapped(const InMap& in, double* x, double* out, double sign, int epi,
+                  const EpiArgs& e, cudaStream_t s) const;
   void apply(const double* x, double* y, cudaStream_t s) const {
     run(x, y, 1.0, EPI_STORE, EpiArgs{}, s);
   }
@@ -84,6 +91,8 @@ class StructuredOp {
   void scale(double s);
 
  private:
+  void run_impl(const InMap* in, const double* x, double* out, double sign, int epi,
+                const EpiArgs& e, cudaStream_t s) const;
   void upload();
   size_t n1_, n2_;
   double inv_r_, s_over_r_;

@@ -214,55 +214,13 @@ __global__ void k_restrict(Xfer t, const double* __restrict__ f, int f_lo,
   }
 }
 
-// 1D prolongation weight accumulation in the reference order: fine index i
-// receives 1.0 * c[j] if i is a coarse point, else 0.5*c[left] then 0.5*c[right].
-__device__ __forceinline__ double prow(const double* c, int k, int i, int par) {
-  // coarse j sits at fine 2j+1-par
-  const int t = i - 1 + par;  // = 2j when i is the coarse point of j
-  if ((t & 1) == 0) {
-    const int j = t >> 1;
-    return (j >= 0 && j < k) ? c[j] : 0.0;  // 0 + 1.0*c
-  }
-  const int jl = (t - 1) >> 1, jr = jl + 1;  // fine i = fc(jl)+1 = fc(jr)-1
-  double v = 0.0;
-  if (jl >= 0 && jl < k) v += 0.5 * c[jl];
-  if (jr >= 0 && jr < k) v += 0.5 * c[jr];
-  return v;
-}
-
 template <bool ADD>
 __global__ void k_prolong(Xfer t, const double* __restrict__ c, int c_lo,
                           double* __restrict__ f, int f_lo, int f_rows) {
   const size_t nf = (size_t)t.n1 * f_rows;
   GRID_STRIDE(q, nf) {
     const int i = (int)(q % t.n1), j = (int)(q / t.n1) + f_lo;  // global fine row
-    auto crow = [&](int r, int width) { return c + (size_t)(r - c_lo) * width; };
-    double v;
-    if (!t.cx) {  // prolong_cols only: rows of width n1 (multigrid.cpp:34-44)
-      const int tt = j - 1 + t.par2;
-      if ((tt & 1) == 0) {
-        const int jc = tt >> 1;
-        v = (jc >= 0 && jc < t.k2) ? crow(jc, t.n1)[i] : 0.0;
-      } else {
-        const int jl = (tt - 1) >> 1, jr = jl + 1;
-        v = 0.0;
-        if (jl >= 0 && jl < t.k2) v += 0.5 * crow(jl, t.n1)[i];
-        if (jr >= 0 && jr < t.k2) v += 0.5 * crow(jr, t.n1)[i];
-      }
-    } else if (!t.cy) {  // prolong_rows only
-      v = prow(crow(j, t.k1), t.k1, i, t.par1);
-    } else {  // rows into tmp (n1 x k2), then columns
-      const int tt = j - 1 + t.par2;
-      if ((tt & 1) == 0) {
-        const int jc = tt >> 1;
-        v = (jc >= 0 && jc < t.k2) ? prow(crow(jc, t.k1), t.k1, i, t.par1) : 0.0;
-      } else {
-        const int jl = (tt - 1) >> 1, jr = jl + 1;
-        v = 0.0;
-        if (jl >= 0 && jl < t.k2) v += 0.5 * prow(crow(jl, t.k1), t.k1, i, t.par1);
-        if (jr >= 0 && jr < t.k2) v += 0.5 * prow(crow(jr, t.k1), t.k1, i, t.par1);
-      }
-    }
+    const double v = prolong_point(t, c, c_lo, i, j);
     if (ADD) f[q] += v;
     else f[q] = v;
   }

@@ -4,6 +4,7 @@
 // Krylov host loop reads them back in one small copy per iteration.
 #pragma once
 #include "devbuf.cuh"
+#include "transfer.cuh"
 
 namespace fde_b200 {
 
@@ -50,11 +51,6 @@ class Reducer {
   DevBuf<unsigned int> counter_;
 };
 
-// GridTransfer (multigrid.cpp:160-227) between an n1 x n2 fine and a k1 x k2
-// coarse grid; cx/cy select the coarsened directions.
-struct Xfer {
-  int n1, n2, k1, k2, par1, par2, cx, cy;
-};
 Xfer make_xfer(int n1, int n2, bool cx, bool cy);
 // coarse = scale-weighted transpose of prolongation (restrict_full: 0.5,
 // restrict_transpose: 1.0), same operation order as restrict_rows/cols.

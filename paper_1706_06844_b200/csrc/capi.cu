@@ -495,8 +495,10 @@ int fde_march_step(fde_march h, const double* source, int source_mode, void* str
     const size_t m = h->m + 1;
     const double* src = h->src.get();
     if (source_mode == 0) {
-      if (h->p.preset && h->p.source_kind != 1) {
-        generate_source_device(h->p, h->g, m, h->src.get(), s);  // bit-identical uniforms
+      if (h->p.preset) {
+        // same counter hash on the device: uniforms bit-identical, Gaussians
+        // within an ulp or two of the host's log/cos (Appendix A of the survey)
+        generate_source_device(h->p, h->g, m, h->src.get(), s);
       } else {
         h->host_src.resize(n);
         sample_source(h->p, h->g, m, h->host_src.data());

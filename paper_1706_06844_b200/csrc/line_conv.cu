@@ -258,6 +258,17 @@ struct Fft {
 #ifndef FDE_PTS
 #define FDE_PTS 16
 #endif
+// points per thread by FFT size: short lines take fewer points per thread,
+// so more threads share a line and the serial butterfly chain shrinks
+#ifndef FDE_PTS_SMALL
+#define FDE_PTS_SMALL 4  // M <= 256
+#endif
+#ifndef FDE_PTS_9
+#define FDE_PTS_9 8
+#endif
+#ifndef FDE_PTS_10
+#define FDE_PTS_10 8
+#endif
 #ifndef FDE_L2_PREFETCH
 #define FDE_L2_PREFETCH 1
 #endif
@@ -270,7 +281,8 @@ struct Fft {
 
 template <int LOGM>
 struct FftShape {
-  static constexpr int P = FDE_PTS;                    // points per thread
+  static constexpr int P =
+      LOGM <= 8 ? FDE_PTS_SMALL : (LOGM == 9 ? FDE_PTS_9 : (LOGM == 10 ? FDE_PTS_10 : FDE_PTS));
   static constexpr int M = 1 << LOGM;
   static constexpr int T = M / P;                      // threads per line
   static constexpr int LPB = T >= 128 ? 1 : 128 / T;   // lines per CTA

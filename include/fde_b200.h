@@ -33,6 +33,11 @@ typedef enum {
   FDE_ENOMEM = 4
 } fde_status;
 
+/* PrecondKind (proj/include/fde/precond.hpp:18; p2_exact and mgm_galerkin are not offered) and mg::CoarseSolve
+ * (proj/include/fde/multigrid.hpp:95) */
+enum { FDE_PRECOND_NONE = 0, FDE_PRECOND_P2 = 1, FDE_PRECOND_MGM = 2 };
+enum { FDE_COARSE_LU = 0, FDE_COARSE_SWEEPS = 1, FDE_COARSE_NONE = 2 };
+
 const char* fde_last_error(void);
 int fde_abi_version(void); /* FDE_B200_ABI_VERSION */
 #define FDE_B200_ABI_VERSION 1

@@ -5,7 +5,11 @@
   compiled by oracle/Makefile; present wherever it was built (it travels to
   the GPU box in the gpurun snapshot), skipped otherwise.
 
-Both expose the same flat entry points (``orc_*`` / ``ref_*``) over one spec
+* ``Adapter`` -- oracle/_ref/libfde_adapter.so: the reference's own gmres and
+  step loop driving libfde_b200.so through fde::LinOp / fde::Precond adapters
+  (the drop-in check of INTEGRATION.md); needs a GPU to call.
+
+Oracle and RefLib expose the same flat entry points (``orc_*`` / ``ref_*``) over one spec
 struct, so a test can run either checker with identical arguments.
 """
 from __future__ import annotations
@@ -21,6 +25,7 @@ ROOT = Path(__file__).resolve().parents[1]
 ORACLE_DIR = ROOT / "oracle"
 ORACLE_SO = ORACLE_DIR / "liboracle.so"
 REF_SO = ORACLE_DIR / "_ref" / "libfde_ref.so"
+ADAPTER_SO = ORACLE_DIR / "_ref" / "libfde_adapter.so"
 
 _P = ctypes.POINTER(ctypes.c_double)
 _I = ctypes.POINTER(ctypes.c_int)
@@ -271,11 +276,32 @@ class RefLib(_Checker):
         return a.reshape(n, n, order="F")
 
 
+class Adapter(_Checker):
+    prefix = "adapter_"
+
+    def gmres(self, s, b, gpu_op: bool, gpu_pc: bool):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.zeros_like(b)
+        it, conv, nh = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        hist = np.zeros(4096)
+        self._call("gmres", ctypes.byref(s), int(gpu_op), int(gpu_pc), _p(b), _p(x),
+                   ctypes.byref(it), ctypes.byref(conv), _p(hist), 4096, ctypes.byref(nh))
+        return x, it.value, bool(conv.value), hist[:nh.value].copy()
+
+    def march(self, s):
+        n1, n2 = dims_of(s)
+        steps = s.steps or CONFIGS[s.cfg if s.cfg else 1][4]
+        u, its, res = np.zeros(n1 * n2), np.zeros(steps, np.int32), np.zeros(steps)
+        self._call("march", ctypes.byref(s), _p(u), its.ctypes.data_as(_I), _p(res))
+        return dict(u=u, its=its, res=res)
+
+
 def build_oracle() -> None:
     """Build oracle/liboracle.so (and oracle/_ref when /root/reference exists)."""
     subprocess.run(["make", "-s", "-C", str(ORACLE_DIR), "oracle"], check=True)
     if Path(os.environ.get("FDE_REFERENCE", "/root/reference/proj")).exists():
         subprocess.run(["make", "-s", "-C", str(ORACLE_DIR), "ref"], check=True)
+        subprocess.run(["make", "-s", "-C", str(ORACLE_DIR), "adapter"], check=True)
 
 
 def oracle() -> Oracle:
@@ -286,3 +312,7 @@ def oracle() -> Oracle:
 
 def reflib() -> RefLib | None:
     return RefLib(REF_SO) if REF_SO.exists() else None
+
+
+def adapter() -> Adapter | None:
+    return Adapter(ADAPTER_SO) if ADAPTER_SO.exists() else None

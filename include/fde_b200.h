@@ -83,13 +83,14 @@ typedef struct {
   double alpha, beta;
   double ax, bx, ay, by;
   double t_final;
-  int time_dependent_coeffs; /* must be 0: time-dependent coefficients are not supported yet */
+  int time_dependent_coeffs; /* re-assemble operator + preconditioner every step (driver.cpp:37-41) */
   int pq;                    /* 0 = (1,0) reference weights, 1 = (1,-1) */
   fde_field_fn d_plus, d_minus, e_plus, e_minus, source;
   fde_initial_fn initial;
   void* ctx;
-  /* BASELINE preset id (1..5) or 0 for a custom problem.  Presets evaluate
-   * coefficients/sources natively (fde_problem_preset fills this struct). */
+  /* BASELINE preset id (1..5), 100 + k for the reference's manufactured
+   * example k (1..3, fde_problem_example), or 0 for a custom problem.  Presets
+   * evaluate coefficients/sources natively (on the device per step). */
   int preset;
   int source_kind; /* presets: 0 U[0,1), 1 1e-2 N(0,1), 2 zero */
   unsigned long long seed;
@@ -101,6 +102,17 @@ typedef struct {
 int fde_problem_preset(int cfg, unsigned long long seed, int source_kind, size_t steps,
                        double tau, fde_problem* out, size_t* n_out, size_t* steps_out);
 /* Grid (problem.cpp:27-48): out[5] = {hx, hy, dt, inv_r, s_over_r} */
+/* make_example_on / make_example (proj/include/fde/problem.hpp:73-79,
+ * proj/src/problem.cpp:172-260): manufactured example which = 1..3 on
+ * [ax,bx] x [ay,by] (example 2 has time-dependent coefficients; t_final = 1;
+ * exact solution known).  fde_problem_example_default uses [0,len]^2, len = 2
+ * for example 1 and 1 otherwise. */
+int fde_problem_example(int which, double alpha, double beta, double ax, double bx, double ay,
+                        double by, fde_problem* out);
+int fde_problem_example_default(int which, double alpha, double beta, fde_problem* out);
+/* error_inf (problem.hpp:69-70): max |u - exact(., t)| over the grid, u HOST */
+int fde_error_inf(const fde_problem* p, size_t n1, size_t n2, size_t steps, double t,
+                  const double* u, double* err);
 int fde_grid(const fde_problem* p, size_t n1, size_t n2, size_t steps, double* out);
 /* assemble_step_operator (problem.hpp:54-55) */
 int fde_assemble_step_operator(const fde_problem* p, size_t n1, size_t n2, size_t steps,

@@ -276,6 +276,14 @@ int ref_march_timed(const ref_spec* s, double* u_out, int* its, double* res, dou
   });
 }
 
+// error_inf (problem.cpp:106-117) of u against the problem's exact solution at t
+int ref_error_inf(const ref_spec* s, const double* u, double t, double* err) {
+  return guarded([&] {
+    const Setup st = make_setup(*s);
+    *err = fde::error_inf(std::vector<double>(u, u + st.g.size()), st.p, st.g, t);
+  });
+}
+
 // The reference's own fde::time_march (driver.cpp:10-69), (1,0) weights only.
 int ref_time_march(const ref_spec* s, double* u_out, int* its, double* res, double* wall) {
   return guarded([&] {

@@ -90,7 +90,23 @@ struct Setup {
   int pq = 0;
 };
 
+// The reference's manufactured examples (cfg 101..103 -> make_example(k),
+// problem.cpp:257-260; defaults of builtin_examples, problem.cpp:262-265;
+// the table command's Grid(p, n, n, n), cli.cpp:172).
+inline Setup make_example_setup(const ref_spec& s) {
+  const int which = s.cfg - 100;
+  const double al = s.alpha > 0 ? s.alpha : 1.8;
+  const double be = s.beta > 0 ? s.beta : (which == 1 ? 1.6 : 1.9);
+  fde::FdeProblem p = fde::make_example(which, al, be);
+  const int n1 = s.n1 > 0 ? s.n1 : 32, n2 = s.n2 > 0 ? s.n2 : n1;
+  const int steps = s.steps > 0 ? s.steps : n1;
+  fde::Grid g(p, static_cast<std::size_t>(n1), static_cast<std::size_t>(n2),
+              static_cast<std::size_t>(steps));
+  return Setup{p, g, 0};
+}
+
 inline Setup make_setup(const ref_spec& s) {
+  if (s.cfg > 100) return make_example_setup(s);
   Cfg c = defaults(s.cfg);
   const int n1 = s.n1 > 0 ? s.n1 : c.n;
   const int n2 = s.n2 > 0 ? s.n2 : c.n;

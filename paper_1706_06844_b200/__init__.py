@@ -91,6 +91,11 @@ _SIGS = {
     "fde_problem_preset": (_c_int, [_c_int, ctypes.c_ulonglong, _c_int, _c_size, _c_dbl,
                                     ctypes.POINTER(_FdeProblem), ctypes.POINTER(_c_size),
                                     ctypes.POINTER(_c_size)]),
+    "fde_problem_example": (_c_int, [_c_int, _c_dbl, _c_dbl, _c_dbl, _c_dbl, _c_dbl, _c_dbl,
+                                     ctypes.POINTER(_FdeProblem)]),
+    "fde_problem_example_default": (_c_int, [_c_int, _c_dbl, _c_dbl, ctypes.POINTER(_FdeProblem)]),
+    "fde_error_inf": (_c_int, [ctypes.POINTER(_FdeProblem), _c_size, _c_size, _c_size, _c_dbl, _P,
+                               ctypes.POINTER(_c_dbl)]),
     "fde_grid": (_c_int, [ctypes.POINTER(_FdeProblem), _c_size, _c_size, _c_size, _P]),
     "fde_assemble_step_operator": (_c_int, [ctypes.POINTER(_FdeProblem), _c_size, _c_size,
                                             _c_size, _c_size, ctypes.POINTER(_c_vp)]),
@@ -254,6 +259,7 @@ class Problem:
     by: float = 1.0
     t_final: float = 1.0
     pq: int = 0
+    time_dependent_coeffs: bool = False
     d_plus: object = None
     d_minus: object = None
     e_plus: object = None
@@ -278,12 +284,37 @@ class Problem:
                    t_final=s.t_final, pq=s.pq, preset=cfg, source_kind=s.source_kind,
                    seed=seed, n=n.value, steps=st.value)
 
+    @classmethod
+    def example(cls, which: int, alpha: float, beta: float, domain=None) -> "Problem":
+        """make_example_on / make_example (problem.cpp:172-260): the reference's
+        manufactured problem 1..3 (example 2: time-dependent coefficients),
+        evaluated natively (device-side per-step re-assembly)."""
+        s = _FdeProblem()
+        lib = load_library()
+        if domain is None:
+            _check(lib.fde_problem_example_default(which, alpha, beta, ctypes.byref(s)))
+        else:
+            ax, bx, ay, by = domain
+            _check(lib.fde_problem_example(which, alpha, beta, ax, bx, ay, by, ctypes.byref(s)))
+        return cls(alpha=s.alpha, beta=s.beta, ax=s.ax, bx=s.bx, ay=s.ay, by=s.by,
+                   t_final=s.t_final, preset=s.preset,
+                   time_dependent_coeffs=bool(s.time_dependent_coeffs))
+
+    def error_inf(self, u, n1: int, n2: int, steps: int, t: float) -> float:
+        """error_inf (problem.hpp:69-70) against the exact solution at time t."""
+        u = np.ascontiguousarray(np.asarray(u, dtype=np.float64))
+        e = _c_dbl()
+        s = self.c_struct()
+        _check(load_library().fde_error_inf(ctypes.byref(s), n1, n2, steps, t, _ptr(u),
+                                            ctypes.byref(e)))
+        return e.value
+
     def c_struct(self) -> _FdeProblem:
         s = _FdeProblem()
         for k in ("alpha", "beta", "ax", "bx", "ay", "by", "t_final", "pq", "preset",
                   "source_kind", "seed"):
             setattr(s, k, getattr(self, k))
-        s.time_dependent_coeffs = 0
+        s.time_dependent_coeffs = int(bool(self.time_dependent_coeffs))
         if not self.preset:
             self._keep.clear()
             for name in ("d_plus", "d_minus", "e_plus", "e_minus", "source"):
@@ -550,6 +581,8 @@ class SolveReport:
     all_converged: bool
     wall_seconds: float
     solution: np.ndarray
+    has_error: bool = False
+    error_inf: float = float("nan")
 
 
 class March:
@@ -605,5 +638,9 @@ def time_march(problem: Problem, n1: int, n2: int, steps: int, cfg: DriverConfig
     _check(load_library().fde_time_march(ctypes.byref(s), n1, n2, steps, ctypes.byref(c), _ptr(u),
                                          its, _ptr(res), ctypes.byref(wall)))
     its_l = [int(v) for v in its]
-    return SolveReport(n1, n2, steps, its_l, res.tolist(), sum(its_l) / max(steps, 1),
-                       bool(all(r <= cfg.tol for r in res)), wall.value, u)
+    rep = SolveReport(n1, n2, steps, its_l, res.tolist(), sum(its_l) / max(steps, 1),
+                      bool(all(r <= cfg.tol for r in res)), wall.value, u)
+    if problem.preset > 100:  # manufactured examples carry the exact solution (driver.cpp:63-66)
+        rep.has_error = True
+        rep.error_inf = problem.error_inf(u, n1, n2, steps, problem.t_final)
+    return rep

@@ -33,7 +33,10 @@ struct fde_march_s {
   Problem p;
   Grid g;
   fde_driver_config cfg;
-  std::shared_ptr<StructuredOp> op;
+  std::shared_ptr<StructuredOp> op;  // coefficients of t^{m-1} when time dependent
+  std::shared_ptr<StructuredOp> next;  // time dependent: the step-m operator
+  size_t next_m = 0;                   // step the next operator / preconditioner hold
+  FieldScratch fields;
   std::shared_ptr<Precond> pc;
   std::unique_ptr<KrylovWorkspace> ws;
   DevBuf<double> u, b, src, x;
@@ -78,10 +81,13 @@ cudaStream_t stream_of(void* s) { return static_cast<cudaStream_t>(s); }
 // fde_problem (C callbacks or preset) -> Problem
 Problem to_problem(const fde_problem* c) {
   need(c != nullptr, "null problem");
-  need(!c->time_dependent_coeffs,
-       "time-dependent coefficients are not supported by this build (SURVEY 8(f) next)");
   Problem p;
-  if (c->preset) {
+  if (c->preset >= 101 && c->preset <= 103) {  // the reference's manufactured examples
+    p = make_example_problem(c->preset - 100, c->alpha, c->beta, c->ax, c->bx, c->ay, c->by);
+    need(c->time_dependent_coeffs == (p.time_dependent_coeffs ? 1 : 0),
+         "example problems fix time_dependent_coeffs (example 2 only)");
+  } else if (c->preset) {
+    need(!c->time_dependent_coeffs, "BASELINE presets have time-independent coefficients");
     p = make_preset(c->preset, c->seed, c->source_kind, 0, 0.0);
   } else {
     need(c->d_plus && c->d_minus && c->e_plus && c->e_minus, "problem is missing a coefficient field");
@@ -108,6 +114,7 @@ Problem to_problem(const fde_problem* c) {
   p.by = c->by;
   p.t_final = c->t_final;
   p.pq = c->pq;
+  if (!c->preset) p.time_dependent_coeffs = c->time_dependent_coeffs != 0;
   need(p.pq == 0 || p.pq == 1, "pq must be 0 ((1,0)) or 1 ((1,-1))");
   return p;
 }
@@ -255,6 +262,39 @@ int fde_problem_preset(int cfg, unsigned long long seed, int source_kind, size_t
     out->seed = seed;
     if (n_out) *n_out = in.n;
     if (steps_out) *steps_out = st;
+  });
+}
+
+int fde_problem_example(int which, double alpha, double beta, double ax, double bx, double ay,
+                        double by, fde_problem* out) {
+  return guard([&] {
+    need(out != nullptr, "null output");
+    const Problem p = make_example_problem(which, alpha, beta, ax, bx, ay, by);  // validates
+    std::memset(out, 0, sizeof *out);
+    out->alpha = alpha;
+    out->beta = beta;
+    out->ax = ax;
+    out->bx = bx;
+    out->ay = ay;
+    out->by = by;
+    out->t_final = p.t_final;
+    out->time_dependent_coeffs = p.time_dependent_coeffs ? 1 : 0;
+    out->preset = 100 + which;
+  });
+}
+
+int fde_problem_example_default(int which, double alpha, double beta, fde_problem* out) {
+  const double len = which == 1 ? 2.0 : 1.0;
+  return fde_problem_example(which, alpha, beta, 0.0, len, 0.0, len, out);
+}
+
+int fde_error_inf(const fde_problem* p, size_t n1, size_t n2, size_t steps, double t,
+                  const double* u, double* err) {
+  return guard([&] {
+    need(u != nullptr && err != nullptr, "null argument");
+    const Problem pr = to_problem(p);
+    const Grid g(pr, n1, n2, steps);
+    *err = error_inf(std::vector<double>(u, u + g.size()), pr, g, t);
   });
 }
 
@@ -473,9 +513,19 @@ int fde_march_create(const fde_problem* p, size_t n1, size_t n2, size_t steps,
     const size_t n = h->g.size();
     // driver.cpp:22-27: u0, operator and preconditioner (time-independent coefficients)
     const std::vector<double> u0 = sample_initial(h->p, h->g);
-    h->op = assemble_step_operator(h->p, h->g, 1);
-    h->pc = make_pc(cfg->precond, h->p, h->g, 1, h->op, cfg->omega, cfg->cycles, cfg->coarse,
-                    cfg->coarse_sweeps);
+    if (h->p.time_dependent_coeffs) {
+      // driver.cpp:23-27,37-41: op holds t^0; the step-1 operator and
+      // preconditioner are built up front and refreshed in place per step
+      h->op = assemble_step_operator(h->p, h->g, 0);
+      h->next = assemble_step_operator(h->p, h->g, 1);
+      h->next_m = 1;
+      h->pc = make_pc(cfg->precond, h->p, h->g, 1, h->next, cfg->omega, cfg->cycles,
+                      cfg->coarse, cfg->coarse_sweeps);
+    } else {
+      h->op = assemble_step_operator(h->p, h->g, 1);
+      h->pc = make_pc(cfg->precond, h->p, h->g, 1, h->op, cfg->omega, cfg->cycles, cfg->coarse,
+                      cfg->coarse_sweeps);
+    }
     h->ws = std::make_unique<KrylovWorkspace>(n, cfg->restart < 5 ? 5 : cfg->restart);
     h->u.upload(u0.data(), n);
     h->b.alloc(n);
@@ -494,8 +544,26 @@ int fde_march_step(fde_march h, const double* source, int source_mode, void* str
     const size_t n = h->g.size();
     const size_t m = h->m + 1;
     const double* src = h->src.get();
+    if (h->p.time_dependent_coeffs && h->next_m != m) {
+      // driver.cpp:37-41: re-assemble the step-m operator and preconditioner
+      refresh_step_operator(*h->next, h->p, h->g, m, h->fields, s);
+      const int kind = h->pc->kind();
+      if (kind == PC_MGM) {
+        Hierarchy* hh = h->pc->mutable_hierarchy();
+        if (!refresh_geometric_hierarchy(*hh, h->p, h->g, m, h->fields, s))
+          h->pc = make_pc(kind, h->p, h->g, m, h->next, h->cfg.omega, h->cfg.cycles,
+                          h->cfg.coarse, h->cfg.coarse_sweeps);  // the level plan moved
+      } else if (kind == PC_P2) {
+        h->next->sync_host(s);  // build_p2 reads the operator's fields
+        h->pc = make_pc(kind, h->p, h->g, m, h->next, h->cfg.omega, h->cfg.cycles,
+                        h->cfg.coarse, h->cfg.coarse_sweeps);
+      }
+      h->next_m = m;
+    }
     if (source_mode == 0) {
-      if (h->p.preset) {
+      if (h->p.example.which) {
+        example_source_device(h->p, h->g, m, h->src.get(), s);
+      } else if (h->p.preset) {
         // same counter hash on the device: uniforms bit-identical, Gaussians
         // within an ulp or two of the host's log/cos (Appendix A of the survey)
         generate_source_device(h->p, h->g, m, h->src.get(), s);
@@ -521,10 +589,12 @@ int fde_march_step(fde_march h, const double* source, int source_mode, void* str
     h->op->run(h->u.get(), h->b.get(), -1.0, EPI_RHS, e, s);
     SolverConfig c{h->cfg.tol, h->cfg.restart, h->cfg.max_outer};
     const Precond* pc = h->pc->kind() == PC_NONE ? nullptr : h->pc.get();
+    const StructuredOp& a = h->p.time_dependent_coeffs ? *h->next : *h->op;
     const KrylovResult r = h->cfg.solver == 1
-                               ? h->ws->bicgstab(*h->op, pc, c, h->b.get(), h->x.get(), s)
-                               : h->ws->gmres(*h->op, pc, c, h->b.get(), h->x.get(), s);
+                               ? h->ws->bicgstab(a, pc, c, h->b.get(), h->x.get(), s)
+                               : h->ws->gmres(a, pc, c, h->b.get(), h->x.get(), s);
     std::swap(h->u, h->x);
+    if (h->p.time_dependent_coeffs) std::swap(h->op, h->next);  // driver.cpp:51
     h->m = m;
     if (iterations) *iterations = r.total_iterations;
     if (residual) *residual = r.residual_history.back();

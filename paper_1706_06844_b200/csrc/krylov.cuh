@@ -27,6 +27,8 @@ class Precond {
   int kind() const { return kind_; }
   size_t size() const { return n_; }
   const Hierarchy* hierarchy() const { return h_.get(); }
+  // in-place refresh of time-dependent levels (captured graphs stay valid)
+  Hierarchy* mutable_hierarchy() const { return h_.get(); }
   // z = cycles V-cycles from z = 0 (precond.cpp:22-26); PC_NONE copies.
   // The whole cycle (~7 launches per level) is captured once per (r, z)
   // pair into a CUDA graph and replayed (FDE_NO_GRAPH=1 disables).

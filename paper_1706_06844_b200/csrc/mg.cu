@@ -187,6 +187,18 @@ Hierarchy::Hierarchy(std::vector<LevelOp> levels, std::vector<std::pair<size_t, 
   }
 }
 
+void Hierarchy::refactor_coarse(cudaStream_t s) {
+  if (coarse_ != COARSE_LU) return;
+  const auto [c1, c2] = dims_.back();
+  if (levels_.back().sop) levels_.back().sop->sync_host(s);
+  std::vector<double> a = dense_of(levels_.back(), c1, c2);
+  std::vector<int> perm;
+  lu_factor(a, c1 * c2, perm);
+  FDE_CUDA(cudaStreamSynchronize(s));
+  lu_.upload(a.data(), a.size());  // same sizes: buffers keep their addresses
+  perm_.upload(perm.data(), perm.size());
+}
+
 void Hierarchy::vcycle(const double* b, double* x, bool zero_guess, cudaStream_t s) const {
   cycle(0, b, x, zero_guess, s);
 }

@@ -59,6 +59,12 @@ class Hierarchy {
   // is all-zero instead of the reference's scan.
   void vcycle(const double* b, double* x, bool zero_guess, cudaStream_t s) const;
 
+  // Per-step refresh of time-dependent levels (refresh_geometric_hierarchy):
+  // the level's dinv buffer (rewritten in place, so captured V-cycle graphs
+  // stay valid) and re-factoring of the dense coarsest level.
+  double* dinv_dev(size_t l) const { return dinv_[l].get(); }
+  void refactor_coarse(cudaStream_t s);
+
  private:
   void cycle(size_t l, const double* b, double* x, bool zero, cudaStream_t s) const;
   std::vector<LevelOp> levels_;

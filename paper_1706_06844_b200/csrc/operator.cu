@@ -170,7 +170,8 @@ StructuredOp::StructuredOp(size_t n1, size_t n2, double inv_r, double s_over_r,
                            ToeplitzDev ax, ToeplitzDev ay, std::vector<double> dp,
                            std::vector<double> dm, std::vector<double> ep,
                            std::vector<double> em)
-    : n1_(n1), n2_(n2), inv_r_(inv_r), s_over_r_(s_over_r), ax_(std::move(ax)),
+    : n1_(n1), n2_(n2), inv_r_(inv_r), s_over_r_(s_over_r), inv_r0_(inv_r),
+      s_over_r0_(s_over_r), ax_(std::move(ax)),
       ay_(std::move(ay)), dp_(std::move(dp)), dm_(std::move(dm)), ep_(std::move(ep)),
       em_(std::move(em)) {
   const size_t n = n1_ * n2_;
@@ -210,6 +211,7 @@ void StructuredOp::upload() {
 }
 
 void StructuredOp::scale(double s) {
+  scales_.push_back(s);
   inv_r_ *= s;
   s_over_r_ *= s;
   for (double& v : dp_) v *= s;
@@ -219,6 +221,84 @@ void StructuredOp::scale(double s) {
   d_dp_.upload(dp_.data(), n);
   d_dm_.upload(dm_.data(), n);
   d_diag_.upload(diag_.data(), n);
+}
+
+namespace {
+
+struct Scales {
+  int n;
+  double v[8];
+};
+
+// Explicitly rounded operations: the same sequence as the host construction
+// (no FMA contraction), so refreshed diagonals equal a fresh host build.
+__global__ void k_refresh(size_t n, double inv_r0, double sr0, double ax0, double ay0,
+                          Scales sc, const double* __restrict__ dp, const double* __restrict__ dm,
+                          const double* __restrict__ ep, const double* __restrict__ em,
+                          double* __restrict__ odp, double* __restrict__ odm,
+                          double* __restrict__ diag, double* __restrict__ dinv, int* flag) {
+  int bad = 0;
+  for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < n;
+       p += (size_t)gridDim.x * blockDim.x) {
+    double a = dp[p], b = dm[p];
+    const double e = ep[p], f = em[p];
+    if (a < 0.0 || b < 0.0 || e < 0.0 || f < 0.0) bad |= 1;
+    // inv_r + (dp + dm) ax0 + s/r (ep + em) ay0   (structured.cpp:119-122)
+    double d = __dadd_rn(inv_r0, __dmul_rn(__dadd_rn(a, b), ax0));
+    d = __dadd_rn(d, __dmul_rn(__dmul_rn(sr0, __dadd_rn(e, f)), ay0));
+    for (int k = 0; k < sc.n; ++k) {  // scale(s): dp, dm, diag *= s
+      a = __dmul_rn(a, sc.v[k]);
+      b = __dmul_rn(b, sc.v[k]);
+      d = __dmul_rn(d, sc.v[k]);
+    }
+    odp[p] = a;
+    odm[p] = b;
+    diag[p] = d;
+    if (dinv) {
+      if (!(d > 0.0)) bad |= 2;
+      dinv[p] = __ddiv_rn(1.0, d);
+    }
+  }
+  if (bad) atomicOr(flag, bad);
+}
+
+}  // namespace
+
+void StructuredOp::refresh(const double* dp, const double* dm, const double* ep,
+                           const double* em, double* dinv, int* flag, cudaStream_t s) {
+  const size_t n = n1_ * n2_;
+  Scales sc{};
+  if (scales_.size() > 8) throw InvalidArgument("too many scale() factors to refresh");
+  sc.n = (int)scales_.size();
+  for (int k = 0; k < sc.n; ++k) sc.v[k] = scales_[k];
+  size_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_refresh<<<(int)blocks, 256, 0, s>>>(n, inv_r0_, s_over_r0_, ax_.first_col()[0],
+                                        ay_.first_col()[0], sc, dp, dm, ep, em, d_dp_.get(),
+                                        d_dm_.get(), d_diag_.get(), dinv, flag);
+  FDE_LAUNCH_CHECK();
+  launch_transpose(ep, d_epT_.get(), (int)n1_, (int)n2_, s);  // column-pass layout
+  launch_transpose(em, d_emT_.get(), (int)n1_, (int)n2_, s);
+  host_stale_ = true;
+}
+
+void StructuredOp::sync_host(cudaStream_t s) {
+  if (!host_stale_) return;
+  const size_t n = n1_ * n2_;
+  std::vector<double> t(n);
+  FDE_CUDA(cudaMemcpyAsync(dp_.data(), d_dp_.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  FDE_CUDA(cudaMemcpyAsync(dm_.data(), d_dm_.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  FDE_CUDA(cudaMemcpyAsync(diag_.data(), d_diag_.get(), n * sizeof(double),
+                           cudaMemcpyDeviceToHost, s));
+  FDE_CUDA(cudaMemcpyAsync(t.data(), d_epT_.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  FDE_CUDA(cudaStreamSynchronize(s));
+  for (size_t j = 0; j < n2_; ++j)
+    for (size_t i = 0; i < n1_; ++i) ep_[i + j * n1_] = t[i * n2_ + j];
+  FDE_CUDA(cudaMemcpyAsync(t.data(), d_emT_.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  FDE_CUDA(cudaStreamSynchronize(s));
+  for (size_t j = 0; j < n2_; ++j)
+    for (size_t i = 0; i < n1_; ++i) em_[i + j * n1_] = t[i * n2_ + j];
+  host_stale_ = false;
 }
 
 bool StructuredOp::maps_input() const {

@@ -90,17 +90,32 @@ class StructuredOp {
   // structured.cpp:154-162
   void scale(double s);
 
+  // Per-step re-assembly for time-dependent coefficients (driver.cpp:37-41,
+  // problem.cpp:50-71): new UNSCALED samples (device arrays) replace the
+  // coefficients, the scale() factors applied so far are re-applied in order,
+  // and the diagonal is recomputed on the device in the reference's order
+  // (structured.cpp:119-122 then 154-162); dinv = 1/diag when dinv is set
+  // (MgHierarchy ctor, multigrid.cpp:306-312).  flag (device int) gets bit 0
+  // for a negative coefficient sample, bit 1 for a nonpositive diagonal.
+  // Host copies (dp(), diagonal(), ...) are stale until sync_host().
+  void refresh(const double* dp, const double* dm, const double* ep, const double* em,
+               double* dinv, int* flag, cudaStream_t s);
+  void sync_host(cudaStream_t s);
+
  private:
   void run_impl(const InMap* in, const double* x, double* out, double sign, int epi,
                 const EpiArgs& e, cudaStream_t s) const;
   void upload();
   size_t n1_, n2_;
   double inv_r_, s_over_r_;
+  double inv_r0_, s_over_r0_;  // as constructed (before scale())
+  std::vector<double> scales_;  // scale() factors in order
   ToeplitzDev ax_, ay_;
   std::vector<double> dp_, dm_, ep_, em_, diag_;
   DevBuf<double> d_dp_, d_dm_, d_epT_, d_emT_, d_diag_;
   mutable DevBuf<double> d_q_, d_xT_;
   bool transpose_columns_ = true;
+  bool host_stale_ = false;
 };
 
 }  // namespace fde_b200

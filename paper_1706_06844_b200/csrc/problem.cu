@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cmath>
 
 #include "problem.cuh"
@@ -229,6 +230,95 @@ std::shared_ptr<Hierarchy> build_p2_hierarchy(const StructuredOp& op, double ome
   }
   return std::make_shared<Hierarchy>(std::move(levels), dims, MODE_GALERKIN, omega, COARSE_NONE,
                                      3);
+}
+
+ExampleSpec make_example_spec(int which, double alpha, double beta, double ax, double bx,
+                              double ay, double by) {
+  if (which < 1 || which > 3) throw InvalidArgument("example index must be 1..3");
+  if (!(alpha > 1.0 && alpha <= 2.0 && beta > 1.0 && beta <= 2.0))
+    throw InvalidArgument("fractional orders must lie in (1, 2]");
+  if (!(bx > ax) || !(by > ay)) throw InvalidArgument("degenerate domain");
+  ExampleSpec s;
+  s.which = which;
+  s.alpha = alpha;
+  s.beta = beta;
+  s.ax = ax;
+  s.bx = bx;
+  s.ay = ay;
+  s.by = by;
+  s.amp = which == 1 ? 16.0 : 1.0;
+  // quartic xi^2 (len - xi)^2 (example 1) / sextic xi^3 (len - xi)^3 profiles
+  auto profile = [which](double len, EndPoly& q) {
+    if (which == 1) {
+      const double c[] = {0.0, 0.0, len * len, -2.0 * len, 1.0};
+      q.n = 5;
+      for (int p = 0; p < q.n; ++p) q.c[p] = c[p];
+    } else {
+      const double c[] = {0.0, 0.0, 0.0, len * len * len, -3.0 * len * len, 3.0 * len, -1.0};
+      q.n = 7;
+      for (int p = 0; p < q.n; ++p) q.c[p] = c[p];
+    }
+  };
+  profile(bx - ax, s.px);
+  profile(by - ay, s.py);
+  auto factors = [](double gamma, EndPoly& q) {  // frac_deriv's per-term constants
+    for (int p = 0; p < q.n; ++p) {
+      q.keep[p] = false;
+      if (q.c[p] == 0.0) continue;
+      const double qq = static_cast<double>(p) + 1.0 - gamma;
+      if (qq <= 0.0 && std::fabs(qq - std::nearbyint(qq)) < 1e-12) continue;
+      q.keep[p] = true;
+      q.f[p] = q.c[p] * std::tgamma(static_cast<double>(p) + 1.0) / std::tgamma(qq);
+      q.e[p] = qq - 1.0;
+    }
+  };
+  factors(alpha, s.px);
+  factors(beta, s.py);
+  if (which == 1) {
+    s.ga = std::tgamma(3.0 - alpha);
+    s.gb = std::tgamma(3.0 - beta);
+  }
+  return s;
+}
+
+Problem make_example_problem(int which, double alpha, double beta, double ax, double bx,
+                             double ay, double by) {
+  const ExampleSpec s = make_example_spec(which, alpha, beta, ax, bx, ay, by);
+  Problem p;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.ax = ax;
+  p.bx = bx;
+  p.ay = ay;
+  p.by = by;
+  p.t_final = 1.0;
+  p.time_dependent_coeffs = which == 2;
+  p.example = s;
+  p.d_plus = [s](double x, double y, double t) { return example_coeff(s, 0, x, y, t); };
+  p.d_minus = [s](double x, double y, double t) { return example_coeff(s, 1, x, y, t); };
+  p.e_plus = [s](double x, double y, double t) { return example_coeff(s, 2, x, y, t); };
+  p.e_minus = [s](double x, double y, double t) { return example_coeff(s, 3, x, y, t); };
+  p.source = [s](double x, double y, double t) { return example_source(s, x, y, t); };
+  p.initial = [s](double x, double y) { return example_initial(s, x, y); };
+  p.exact = [s](double x, double y, double t) { return example_exact(s, x, y, t); };
+  return p;
+}
+
+Problem make_example_default(int which, double alpha, double beta) {
+  const double len = which == 1 ? 2.0 : 1.0;
+  return make_example_problem(which, alpha, beta, 0.0, len, 0.0, len);
+}
+
+double error_inf(const std::vector<double>& u, const Problem& p, const Grid& g, double t) {
+  if (!p.exact) throw InvalidArgument("problem has no exact solution");
+  if (u.size() != g.size()) throw InvalidArgument("size mismatch");
+  double e = 0.0;
+  for (size_t j = 0; j < g.n2; ++j)
+    for (size_t i = 0; i < g.n1; ++i) {
+      const double ref = p.exact(g.x(i), g.y(j), t);
+      e = std::max(e, std::fabs(u[i + j * g.n1] - ref));
+    }
+  return e;
 }
 
 PresetInfo preset_info(int cfg) {

@@ -7,6 +7,7 @@
 #include <memory>
 #include <vector>
 
+#include "examples.cuh"
 #include "mg.cuh"
 
 namespace fde_b200 {
@@ -23,6 +24,10 @@ struct Problem {
   int preset = 0;
   int source_kind = 0;  // 0 U[0,1), 1 1e-2 N(0,1), 2 zero
   uint64_t seed = 0;
+  // reference manufactured example (make_example_on) when example.which != 0:
+  // coefficients / sources / exact solution also evaluable on the device
+  ExampleSpec example;
+  std::function<double(double, double, double)> exact;  // may be empty
 };
 
 struct Grid {  // problem.cpp:27-48
@@ -54,6 +59,48 @@ std::shared_ptr<Hierarchy> build_geometric_hierarchy(const Problem& p, const Gri
 // P2VcyclePrecond hierarchy: build_p2 (precond.cpp:50-73) + Galerkin R A P
 // levels (multigrid.cpp:443-475), coarsest CoarseSolve::none.
 std::shared_ptr<Hierarchy> build_p2_hierarchy(const StructuredOp& fine, double omega);
+
+// make_example_on (problem.cpp:172-255): the manufactured problems 1..3
+// (example 2 has time-dependent coefficients); t_final = 1.
+Problem make_example_problem(int which, double alpha, double beta, double ax, double bx,
+                             double ay, double by);
+// make_example (problem.cpp:257-260): [0, len]^2 with len 2 for example 1, else 1
+Problem make_example_default(int which, double alpha, double beta);
+// error_inf (problem.cpp:106-117): max |u - exact(., t)|, exact sampled on the host
+double error_inf(const std::vector<double>& u, const Problem& p, const Grid& g, double t);
+
+// Coefficient fields of step m (t = m dt) on grid g into DEVICE arrays,
+// unscaled: on the device for example problems, else host callbacks + upload.
+void sample_fields_device(const Problem& p, const Grid& g, size_t m, double* dp, double* dm,
+                          double* ep, double* em, cudaStream_t s);
+// v(x_i, y_j, t^{m-1/2}) of an example problem on the device
+void example_source_device(const Problem& p, const Grid& g, size_t m, double* v,
+                           cudaStream_t s);
+
+// Device scratch for one level's four coefficient fields.
+struct FieldScratch {
+  DevBuf<double> dp, dm, ep, em, partial;
+  DevBuf<int> flag;
+  void ensure(size_t n);
+};
+
+// anisotropy_ratio (multigrid.cpp:116-128) of a fine operator whose UNSCALED
+// fields sit in `f` (deterministic device sums; the reference sums
+// sequentially, so the ratio can differ in the last bits).
+double anisotropy_ratio_device(FieldScratch& f, size_t n, double s_over_r, double alpha,
+                               double beta, cudaStream_t s);
+
+// Time-dependent re-assembly of a geometric hierarchy at step m in place
+// (driver.cpp:37-41 rebuilds it; multigrid.cpp:407-441 is what it rebuilds):
+// every level's coefficients re-sampled on its own grid and refreshed with
+// its fine-level scaling, dinv and the coarsest LU updated.  Returns false
+// (nothing changed) when the step-m level plan differs from the hierarchy's;
+// the caller then builds a new hierarchy.
+bool refresh_geometric_hierarchy(Hierarchy& h, const Problem& p, const Grid& g, size_t m,
+                                 FieldScratch& f, cudaStream_t s);
+// The step operator itself (assemble_step_operator at step m) in place.
+void refresh_step_operator(StructuredOp& op, const Problem& p, const Grid& g, size_t m,
+                           FieldScratch& f, cudaStream_t s);
 
 // BASELINE configurations: coefficient fields,
 // u0 = x^2(1-x)^2 y^2(1-y)^2, counter-hash seeded sources.

@@ -12,6 +12,7 @@
 #include <type_traits>
 
 #include "line_conv.cuh"
+#include "tmem.cuh"
 
 namespace fde_b200 {
 namespace {
@@ -352,8 +353,8 @@ __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
     const int qm = swz<SH>((M - k) & (M - 1));
     const double zr = v[s].x, zi = v[s].y;
     const double mr = ra[qm], mi = ia[qm];
-    const double2* abk = reinterpret_cast<const double2*>(p.blk.ab) + 2 * k;
-    const double2 ca = __ldg(abk), cb = __ldg(abk + 1);  // a_k, b_k
+    const double2* abk = reinterpret_cast<const double2*>(p.blk.ab) + k;
+    const double2 ca = __ldg(abk), cb = __ldg(abk + M);  // a_k, b_k
     const double t1 = ca.x * zr, t2 = ca.y * zi, t3 = ca.x * zi, t4 = ca.y * zr;
     const double u1 = cb.x * mr, u2 = cb.y * mi, u3 = cb.y * mr, u4 = cb.x * mi;
     v[s] = make_double2((t1 - t2) + (u1 + u2), (t3 + t4) + (u3 - u4));
@@ -399,6 +400,443 @@ __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
       if (i0 + 1 < n) p.finish(line, i0 + 1, ty[s].y, v[s].y, o[2 * (s - g) + 1]);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Paired-spectrum line kernel (M = 2^LOGM with LOGM % log2(P) != 0).
+//
+// The forward transform runs its radix-P stages first and the short radix
+// R0 = 2^(LOGM mod log2 P) stage last; the two inverses run R0 first.  The
+// last forward stage hands thread tl the butterflies {j, NS0 - j} (thread 0:
+// the self-paired 0 and NS0/2), so every Z[k] and its spectral partner
+// Z[M - k] sit in the same thread's registers, and the first inverse stage
+// (radix R0, stride NS0) reads exactly those slots: no shared-memory round
+// trip between the forward transform, the spectral step and the inverses.
+// The packed spectra Qy, Qt and the first inverse's output are parked in
+// tensor memory (tmem.cuh), so registers hold one 16-point set per thread and
+// three CTAs share an SM.  Exchange buffers alternate (one barrier per
+// exchange).
+#ifndef FDE_PAIRED_DBUF
+#define FDE_PAIRED_DBUF 0
+#endif
+template <int LOGM, int P>
+struct PairedShape {
+  static constexpr int M = 1 << LOGM, T = M / P, LP = Log2<P>::v;
+  static constexpr int REM = LOGM % LP;  // log2 R0
+  static constexpr int R0 = 1 << REM;
+  static constexpr int B0 = P / R0;      // butterflies per thread in the R0 stage
+  static constexpr int NS0 = M / R0;     // = B0 * T
+  static constexpr int THREADS = T;
+  static constexpr int BUF = M;          // doubles per re / im plane
+  // alternating exchange buffers need an even exchange count per transform
+  // (both inverses start on buffer 0 with no barrier in between)
+  static constexpr int NBUF = (FDE_PAIRED_DBUF && (LOGM / LP) % 2 == 0) ? 2 : 1;
+  static constexpr size_t SMEM = size_t(NBUF) * 2 * BUF * sizeof(double);
+  static constexpr int TCOLS = 8 * P;    // Qy (4P words) + Qt (4P words) per thread
+  static_assert(REM != 0, "paired kernel needs a short stage");
+  static_assert(T % 32 == 0 && T <= 128, "one lane quadrant per warp");
+};
+
+#ifndef FDE_PAIRED_MINB
+#define FDE_PAIRED_MINB 4  // CTAs per SM at M = 2048 (128 registers)
+#endif
+#ifndef FDE_PAIRED_MINB10
+#define FDE_PAIRED_MINB10 5
+#endif
+
+// butterfly handled in slot q of the paired R0 stage
+template <int B, int T>
+__device__ __forceinline__ int paired_bfly(int tl, int q) {
+  constexpr int NS = B * T;
+  if (tl == 0) return q * T;
+  return q < B / 2 ? tl + q * T : NS - tl - (q - B / 2) * T;
+}
+
+// twiddle + DFT of this thread's B = P / R butterflies (slots q + r * B)
+template <int LOGM, int P, bool INV, int NSL, int R, bool PAIRED, bool HALF>
+__device__ __forceinline__ void pstage_compute(double2 (&v)[P], int tl, const double2 (&w1s)[P]) {
+  constexpr int B = P / R, NS = 1 << NSL;
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    double2 u[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) u[r] = v[q + r * B];
+    if constexpr (NS > 1) {
+      double2 w1 = w1s[q];
+      if (INV) w1.y = -w1.y;
+      double2 w[R];
+      powers<R>(w1, w);
+#pragma unroll
+      for (int r = 1; r < R; ++r) u[r] = cmul(u[r], w[r]);
+    }
+    Dft<R, INV, HALF>::run(u);
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[q + r * B] = u[r];
+  }
+}
+
+template <int LOGM, int P, int NSL, int R, bool PAIRED>
+__device__ __forceinline__ void pstage_twiddles(double2 (&w1s)[P], int tl, const double2* twM) {
+  constexpr int T = (1 << LOGM) / P, B = P / R, NS = 1 << NSL;
+  constexpr int TWSH = LOGM - NSL - Log2<R>::v;
+  if constexpr (NS > 1) {
+#pragma unroll
+    for (int q = 0; q < B; ++q) {
+      const int j = PAIRED ? paired_bfly<B, T>(tl, q) : tl + q * T;
+      w1s[q] = twM[(j & (NS - 1)) << TWSH];
+    }
+  }
+}
+
+// Stockham write of a finished stage (NSL, R) to plane (re, im)
+template <int LOGM, int P, int NSL, int R, bool PAIRED>
+__device__ __forceinline__ void pstage_write(const double2 (&v)[P], double* re, double* im,
+                                             int tl) {
+  constexpr int T = (1 << LOGM) / P, B = P / R, NS = 1 << NSL, SH = Log2<P>::v;
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    const int j = PAIRED ? paired_bfly<B, T>(tl, q) : tl + q * T;
+    const int base = ((j >> NSL) << (NSL + Log2<R>::v)) + (j & (NS - 1));
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int p = swz<SH>(base + r * NS);
+      re[p] = v[q + r * B].x;
+      im[p] = v[q + r * B].y;
+    }
+  }
+}
+
+// inputs of stage (R, PAIRED): butterfly j reads j + r * M / R
+template <int LOGM, int P, int R, bool PAIRED>
+__device__ __forceinline__ void pstage_read(double2 (&v)[P], const double* re, const double* im,
+                                            int tl) {
+  constexpr int M = 1 << LOGM, T = M / P, B = P / R, SH = Log2<P>::v;
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    const int j = PAIRED ? paired_bfly<B, T>(tl, q) : tl + q * T;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int p = swz<SH>(j + r * (M / R));
+      v[q + r * B] = make_double2(re[p], im[p]);
+    }
+  }
+}
+
+// Forward transform, radix-P stages from NSL, ending with the paired R0 stage.
+// On entry the stage at NSL has its inputs in v; the exchange buffer toggles.
+template <int LOGM, int P, int NSL, bool HALF>
+struct PFwd {
+  __device__ __forceinline__ static void run(double2 (&v)[P], double* buf, int& cur, int tl,
+                                             const double2* twM, double2 (&w1s)[P]) {
+    using S = PairedShape<LOGM, P>;
+    constexpr int LP = S::LP;
+    static_assert(LOGM - NSL >= LP, "");
+    pstage_compute<LOGM, P, false, NSL, P, false, HALF>(v, tl, w1s);
+    double* re = buf + cur * 2 * S::BUF;
+    if constexpr (S::NBUF == 1) __syncthreads();
+    pstage_write<LOGM, P, NSL, P, false>(v, re, re + S::BUF, tl);
+    constexpr int NX = NSL + LP;
+    constexpr bool LASTP = (LOGM - NX) < LP;  // next stage is the paired R0 stage
+    if constexpr (LASTP) {
+      pstage_twiddles<LOGM, P, NX, S::R0, true>(w1s, tl, twM);
+      __syncthreads();
+      pstage_read<LOGM, P, S::R0, true>(v, re, re + S::BUF, tl);
+      cur ^= S::NBUF - 1;
+      pstage_compute<LOGM, P, false, NX, S::R0, true, false>(v, tl, w1s);
+    } else {
+      pstage_twiddles<LOGM, P, NX, P, false>(w1s, tl, twM);
+      __syncthreads();
+      pstage_read<LOGM, P, P, false>(v, re, re + S::BUF, tl);
+      cur ^= S::NBUF - 1;
+      PFwd<LOGM, P, NX, false>::run(v, buf, cur, tl, twM, w1s);
+    }
+  }
+};
+
+// Inverse radix-P stages from NSL (inputs in v); the last stays in registers.
+template <int LOGM, int P, int NSL>
+struct PInvTail {
+  __device__ __forceinline__ static void run(double2 (&v)[P], double* buf, int& cur, int tl,
+                                             const double2* twM, double2 (&w1s)[P]) {
+    using S = PairedShape<LOGM, P>;
+    constexpr int LP = S::LP;
+    pstage_compute<LOGM, P, true, NSL, P, false, false>(v, tl, w1s);
+    if constexpr (NSL + LP < LOGM) {
+      double* re = buf + cur * 2 * S::BUF;
+      if constexpr (S::NBUF == 1) __syncthreads();
+      pstage_write<LOGM, P, NSL, P, false>(v, re, re + S::BUF, tl);
+      pstage_twiddles<LOGM, P, NSL + LP, P, false>(w1s, tl, twM);
+      __syncthreads();
+      pstage_read<LOGM, P, P, false>(v, re, re + S::BUF, tl);
+      cur ^= S::NBUF - 1;
+      PInvTail<LOGM, P, NSL + LP>::run(v, buf, cur, tl, twM, w1s);
+    }
+  }
+};
+
+// Full inverse: paired R0 stage (NS = 1) on the spectral slots, then radix P.
+template <int LOGM, int P>
+__device__ __forceinline__ void pinverse(double2 (&v)[P], double* buf, int& cur, int tl,
+                                         const double2* twM, double2 (&w1s)[P]) {
+  using S = PairedShape<LOGM, P>;
+  pstage_compute<LOGM, P, true, 0, S::R0, true, false>(v, tl, w1s);
+  double* re = buf + cur * 2 * S::BUF;
+  if constexpr (S::NBUF == 1) __syncthreads();
+  pstage_write<LOGM, P, 0, S::R0, true>(v, re, re + S::BUF, tl);
+  pstage_twiddles<LOGM, P, S::REM, P, false>(w1s, tl, twM);
+  __syncthreads();
+  pstage_read<LOGM, P, P, false>(v, re, re + S::BUF, tl);
+  cur ^= S::NBUF - 1;
+  PInvTail<LOGM, P, S::REM>::run(v, buf, cur, tl, twM, w1s);
+}
+
+// spectral partner slot of slot s = q + r * B0 (tl != 0 / tl == 0)
+template <int B, int R>
+constexpr int partner_slot(int s, bool t0) {
+  const int q = s % B, r = s / B;
+  if (!t0) return (q + B / 2) % B + (R - 1 - r) * B;
+  const int q2 = (B - q) % B;
+  const int r2 = q == 0 ? (R - r) % R : R - 1 - r;
+  return q2 + r2 * B;
+}
+
+// Per-line I/O views for the paired kernel: pointers are offset to the
+// thread's first position 2*tl once, so every slot's accesses use
+// compile-time displacements d = pos - 2*tl (no per-access 64-bit index math).
+template <class Pol, int EPI>
+struct LineIO;
+
+// YPass: EPI carries the layout flags, bit 0 = xT (x transposed), bit 1 = qT
+template <int EPI>
+struct LineIO<YPass, EPI> {
+  static constexpr bool XT = EPI & 1, QT = (EPI >> 1) & 1;
+  const double* x;
+  const double* ep;
+  const double* em;
+  double* q;
+  int n1;
+  double c;
+  struct Ops {
+    double ep, em;
+  };
+  __device__ __forceinline__ LineIO(const YPass& p, int line, int pos0) {
+    const size_t n1s = p.n1, n2 = p.n2;
+    n1 = p.n1;
+    x = XT ? p.x + line * n2 + pos0 : p.x + line + pos0 * n1s;
+    ep = p.epT + line * n2 + pos0;
+    em = p.emT + line * n2 + pos0;
+    q = QT ? p.q + line * n2 + pos0 : p.q + line + pos0 * n1s;
+    c = p.c;
+  }
+  __device__ __forceinline__ double load(int d) const {
+    return XT ? x[d] : x[(size_t)d * n1];
+  }
+  __device__ __forceinline__ Ops fetch(int d) const { return Ops{ep[d], em[d]}; }
+  __device__ __forceinline__ void finish(int d, double ty, double tt, const Ops& o) const {
+    const double v = c * (o.ep * ty + o.em * tt);
+    if (QT) q[d] = v;
+    else q[(size_t)d * n1] = v;
+  }
+};
+
+template <int EPI>
+struct LineIO<XPass, EPI> {
+  const double* x;
+  const double* dp;
+  const double* dm;
+  const double* q;
+  const double* e1;  // src (RHS) or b (RESID / JACOBI)
+  const double* e2;  // dinv (JACOBI)
+  double* out;
+  double inv_r, sign, s2;  // s2: src_scale (RHS) or omega (JACOBI)
+  struct Ops {
+    double x, dp, dm, q, e1, e2;
+  };
+  __device__ __forceinline__ LineIO(const XPass& p, int line, int pos0) {
+    const size_t o = (size_t)line * p.n1 + pos0;
+    x = p.x + o;
+    dp = p.dp + o;
+    dm = p.dm + o;
+    q = p.q ? p.q + o : nullptr;
+    e1 = EPI == EPI_RHS ? p.src + o : (EPI == EPI_STORE ? nullptr : p.b + o);
+    e2 = EPI == EPI_JACOBI ? p.dinv + o : nullptr;
+    out = p.out + o;
+    inv_r = p.inv_r;
+    sign = p.sign;
+    s2 = EPI == EPI_RHS ? p.src_scale : p.omega;
+  }
+  __device__ __forceinline__ double load(int d) const { return x[d]; }
+  __device__ __forceinline__ Ops fetch(int d) const {
+    Ops o;
+    o.x = x[d];
+    o.dp = dp[d];
+    o.dm = dm[d];
+    o.q = q ? q[d] : 0.0;
+    o.e1 = EPI == EPI_STORE ? 0.0 : e1[d];
+    o.e2 = EPI == EPI_JACOBI ? e2[d] : 0.0;
+    return o;
+  }
+  __device__ __forceinline__ void finish(int d, double ty, double tt, const Ops& o) const {
+    // structured.cpp:128,134-135,146: y = inv_r x; y += s dp t; y += s dm tt; y += Q
+    double y = inv_r * o.x;
+    y += sign * o.dp * ty;
+    y += sign * o.dm * tt;
+    if (q) y += o.q;
+    if constexpr (EPI == EPI_RHS) out[d] = y + s2 * o.e1;
+    else if constexpr (EPI == EPI_RESID) out[d] = o.e1 - y;
+    else if constexpr (EPI == EPI_JACOBI) out[d] = o.x + s2 * o.e2 * (o.e1 - y);
+    else out[d] = y;
+  }
+};
+
+template <int LOGM, class Pol, int EPI>
+__global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THREADS,
+                                  LOGM >= 11 ? FDE_PAIRED_MINB : FDE_PAIRED_MINB10)
+    fft_line_kernel_paired(const Pol p) {
+  constexpr int P = LOGM >= 11 ? 16 : 8;
+  using S = PairedShape<LOGM, P>;
+  constexpr int T = S::T, H = P / 2, R0 = S::R0, B0 = S::B0, NS0 = S::NS0;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ uint32_t s_tbase;
+  const int tl = threadIdx.x, warp = tl >> 5;
+  const int line = blockIdx.x;
+  const int n = p.blk.n;
+
+  if (warp == 0) tmem_alloc<S::TCOLS>(&s_tbase);
+#if FDE_L2_PREFETCH
+  for (int c = tl; c * 16 < n; c += T) p.prefetch(line, c);
+#endif
+
+  // 1) z_m = x_2m + i x_2m+1, m = tl + s*T; zero padded (n <= M: s < P/2 only).
+  //    Slot s needs guards only when its last thread's positions reach n.
+  const LineIO<Pol, EPI> io(p, line, 2 * tl);
+  double2 v[P];
+#pragma unroll
+  for (int s = 0; s < H; ++s) {
+    const int i0 = 2 * (tl + s * T), d = 2 * s * T;
+#ifdef FDE_EXP_NOX
+    v[s].x = 1.0 / (i0 + 1);
+    v[s].y = 1.0 / (i0 + 2);
+#else
+    if (2 * T * (s + 1) <= n) {
+      v[s].x = io.load(d);
+      v[s].y = io.load(d + 1);
+    } else {
+      v[s].x = i0 < n ? io.load(d) : 0.0;
+      v[s].y = i0 + 1 < n ? io.load(d + 1) : 0.0;
+    }
+#endif
+    v[s + H] = make_double2(0.0, 0.0);
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tq = s_tbase + ((uint32_t)(warp * 32) << 16);  // this warp's lane quadrant
+  const uint32_t tqy = tq, tqt = tq + 4 * P;                    // Qy, Qt column ranges
+
+  // 2) forward transform; ends with this thread's paired slots in v
+  double2 w1s[P];
+  int cur = 0;
+  PFwd<LOGM, P, 0, true>::run(v, smem, cur, tl, p.blk.twM, w1s);
+
+  // 3) spectral step (see fft_line_kernel): partners are in registers; results
+  //    go to tensor memory in groups of 4 slots
+  {
+    const bool t0 = tl == 0;
+    const double2* abv = reinterpret_cast<const double2*>(p.blk.ab);
+#pragma unroll
+    for (int g = 0; g < P; g += 4) {
+      double2 qy[4], qt[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int s = g + c, q = s % B0, r = s / B0;
+        const int k = paired_bfly<B0, T>(tl, q) + r * NS0;
+        constexpr int dummy = 0;
+        (void)dummy;
+        const double2 z = v[s];
+        const double2 zm0 = v[partner_slot<B0, R0>(s, true)];
+        const double2 zm1 = v[partner_slot<B0, R0>(s, false)];
+        const double mr = t0 ? zm0.x : zm1.x, mi = t0 ? zm0.y : zm1.y;
+#ifdef FDE_EXP_NOAB
+        const double2 ca = make_double2(1.0 + k, 0.5), cb = make_double2(0.25, 0.125 * k);
+#else
+        const double2 ca = __ldg(abv + k), cb = __ldg(abv + S::M + k);
+#endif
+        const double t1 = ca.x * z.x, t2 = ca.y * z.y, t3 = ca.x * z.y, t4 = ca.y * z.x;
+        const double u1 = cb.x * mr, u2 = cb.y * mi, u3 = cb.y * mr, u4 = cb.x * mi;
+        qy[c] = make_double2((t1 - t2) + (u1 + u2), (t3 + t4) + (u3 - u4));
+        qt[c] = make_double2((t1 + t2) + (u2 - u1), (t3 - t4) + (u3 + u4));
+      }
+      tmem_st4(tqy + 4 * g, qy);
+      tmem_st4(tqt + 4 * g, qt);
+    }
+  }
+  tmem_wait_st();
+
+  // 4) inverse of Qy -> T x (packed; its H output slots are parked in the Qy
+  //    columns), then 5) inverse of Qt -> T^T x.  One copy of the inverse code
+  //    (instruction-cache footprint): both start on exchange buffer 0.
+  const int n_inv = 2 + (n < 0);  // opaque trip count: ptxas keeps the loop rolled
+#pragma unroll 1
+  for (int it = 0; it < n_inv; ++it) {
+    const uint32_t src = it ? tqt : tqy;
+#pragma unroll
+    for (int g = 0; g < P; g += 4) {
+      double2 t[4];
+      tmem_ld4(src + 4 * g, t);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[g + c] = t[c];
+    }
+    cur = 0;
+    pinverse<LOGM, P>(v, smem, cur, tl, p.blk.twM, w1s);
+    if (it == 0) {
+#pragma unroll
+      for (int g = 0; g < H; g += 4) {
+        double2 t[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) t[c] = v[g + c];
+        tmem_st4(tqy + 4 * g, t);
+      }
+      tmem_wait_st();
+    }
+  }
+
+  // 6) epilogue in groups of 4 slots (8 positions)
+#pragma unroll
+  for (int g = 0; g < H; g += 4) {
+    double2 ty[4];
+    tmem_ld4(tqy + 4 * g, ty);
+    typename LineIO<Pol, EPI>::Ops o[8];
+    if (2 * T * (g + 4) <= n) {  // whole group in range for every thread (uniform)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int d = 2 * (g + c) * T;
+#ifdef FDE_EXP_NOEPI
+        o[2 * c] = typename LineIO<Pol, EPI>::Ops{};
+        o[2 * c + 1] = typename LineIO<Pol, EPI>::Ops{};
+#else
+        o[2 * c] = io.fetch(d);
+        o[2 * c + 1] = io.fetch(d + 1);
+#endif
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int d = 2 * (g + c) * T;
+        io.finish(d, ty[c].x, v[g + c].x, o[2 * c]);
+        io.finish(d + 1, ty[c].y, v[g + c].y, o[2 * c + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
+        if (i0 < n) io.finish(d, ty[c].x, v[g + c].x, io.fetch(d));
+        if (i0 + 1 < n) io.finish(d + 1, ty[c].y, v[g + c].y, io.fetch(d + 1));
+      }
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<S::TCOLS>(s_tbase);
 }
 
 // Warp-per-line direct Toeplitz product for short lines (n <= kDirectMax):
@@ -527,6 +965,43 @@ void launch_fft(const P& p, cudaStream_t s) {
   FDE_LAUNCH_CHECK();
 }
 
+#ifndef FDE_PAIRED
+#define FDE_PAIRED 1
+#endif
+
+template <int LOGM, class P, int EPI>
+void launch_paired_epi(const P& p, cudaStream_t s) {
+  constexpr int PP = LOGM >= 11 ? 16 : 8;
+  using S = PairedShape<LOGM, PP>;
+  static bool configured = false;
+  if (!configured) {
+    FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+    configured = true;
+  }
+  fft_line_kernel_paired<LOGM, P, EPI><<<lines_of(p), S::THREADS, S::SMEM, s>>>(p);
+  FDE_LAUNCH_CHECK();
+}
+
+template <int LOGM, class P>
+void launch_paired(const P& p, cudaStream_t s) {
+  if constexpr (std::is_same<P, YPass>::value) {
+    switch ((p.xT ? 1 : 0) | (p.qT ? 2 : 0)) {
+      case 1: return launch_paired_epi<LOGM, P, 1>(p, s);
+      case 2: return launch_paired_epi<LOGM, P, 2>(p, s);
+      case 3: return launch_paired_epi<LOGM, P, 3>(p, s);
+      default: return launch_paired_epi<LOGM, P, 0>(p, s);
+    }
+  } else {
+    switch (p.epi) {
+      case EPI_RHS: return launch_paired_epi<LOGM, P, EPI_RHS>(p, s);
+      case EPI_RESID: return launch_paired_epi<LOGM, P, EPI_RESID>(p, s);
+      case EPI_JACOBI: return launch_paired_epi<LOGM, P, EPI_JACOBI>(p, s);
+      default: return launch_paired_epi<LOGM, P, EPI_STORE>(p, s);
+    }
+  }
+}
+
 template <class P>
 void launch_any(const P& p, cudaStream_t s) {
   const int lines = lines_of(p);
@@ -540,8 +1015,8 @@ void launch_any(const P& p, cudaStream_t s) {
     case 7: return launch_fft<7>(p, s);
     case 8: return launch_fft<8>(p, s);
     case 9: return launch_fft<9>(p, s);
-    case 10: return launch_fft<10>(p, s);
-    case 11: return launch_fft<11>(p, s);
+    case 10: return FDE_PAIRED ? launch_paired<10>(p, s) : launch_fft<10>(p, s);
+    case 11: return FDE_PAIRED ? launch_paired<11>(p, s) : launch_fft<11>(p, s);
     case 12: return launch_fft<12>(p, s);
     default: throw InvalidArgument("line length beyond the supported FFT sizes");
   }

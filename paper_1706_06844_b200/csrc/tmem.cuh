@@ -1,0 +1,73 @@
+// Tensor-memory (TMEM) per-thread stash for the line kernels.
+//
+// The 32x32b shape maps TMEM lane (32 * (warp % 4) + lane) to the thread, so
+// each thread owns a private row of 32-bit columns.  The FFT line kernels park
+// the spectra and the first inverse's output there instead of in registers:
+// the register file then holds one 16-point transform per thread and the SM
+// keeps three line CTAs resident instead of two.  All tcgen05 instructions
+// here are .sync.aligned: every lane of the warp must execute them.
+#pragma once
+#include <cstdint>
+
+namespace fde_b200 {
+
+__device__ __forceinline__ uint32_t smem_addr_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// warp-wide: allocate NCOL columns, address written to *dst (shared memory)
+template <int NCOL>
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+               ::"r"(smem_addr_u32(dst)), "n"(NCOL));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+template <int NCOL>
+__device__ __forceinline__ void tmem_dealloc(uint32_t base) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(NCOL));
+}
+__device__ __forceinline__ void tmem_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// 4 complex doubles (16 columns) at column offset `taddr`
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const double2 (&v)[4]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(__double2loint(v[0].x)), "r"(__double2hiint(v[0].x)), "r"(__double2loint(v[0].y)),
+      "r"(__double2hiint(v[0].y)), "r"(__double2loint(v[1].x)), "r"(__double2hiint(v[1].x)),
+      "r"(__double2loint(v[1].y)), "r"(__double2hiint(v[1].y)), "r"(__double2loint(v[2].x)),
+      "r"(__double2hiint(v[2].x)), "r"(__double2loint(v[2].y)), "r"(__double2hiint(v[2].y)),
+      "r"(__double2loint(v[3].x)), "r"(__double2hiint(v[3].x)), "r"(__double2loint(v[3].y)),
+      "r"(__double2hiint(v[3].y))
+      : "memory");
+}
+// load + wait in one asm statement, so no consumer can be scheduled between
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, double2 (&v)[4]) {
+  int r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    v[c] = make_double2(__hiloint2double(r[4 * c + 1], r[4 * c]),
+                        __hiloint2double(r[4 * c + 3], r[4 * c + 2]));
+}
+
+}  // namespace fde_b200

@@ -29,7 +29,8 @@ def problem_for(cfg, **kw):
 
 @pytest.mark.parametrize("n1,n2", [(7, 5), (8, 8), (31, 33), (33, 31), (63, 63), (64, 65),
                                    (127, 1), (1, 15), (255, 255), (100, 257), (1023, 15),
-                                   (513, 64), (2047, 3)])
+                                   (513, 64), (2047, 3), (1025, 17), (17, 1025),
+                                   (2048, 5), (5, 2048), (1531, 601), (601, 1531)])
 @pytest.mark.parametrize("sign", [1, -1])
 def test_operator_apply_matches_oracle(cuda, orc, n1, n2, sign):
     s = spec(2, n1=n1, n2=n2, steps=4)

@@ -431,9 +431,13 @@ struct PairedShape {
   // alternating exchange buffers need an even exchange count per transform
   // (both inverses start on buffer 0 with no barrier in between)
   static constexpr int NBUF = (FDE_PAIRED_DBUF && (LOGM / LP) % 2 == 0) ? 2 : 1;
-  static constexpr size_t SMEM = size_t(NBUF) * 2 * BUF * sizeof(double);
+  // exchange buffer(s) + the next line's input (BUF doubles)
+  static constexpr size_t SMEM = (size_t(NBUF) * 2 + 1) * BUF * sizeof(double);
   static constexpr int TCOLS = 8 * P;    // Qy (4P words) + Qt (4P words) per thread
   static_assert(REM != 0, "paired kernel needs a short stage");
+  static constexpr int KX = LP;                 // radix-P -> radix-P exchanges
+  static constexpr int KPF = 0;                 // into the paired forward stage
+  static constexpr int KPI = P == 16 ? 3 : 2;   // out of the paired inverse stage
   static_assert(T % 32 == 0 && T <= 128, "one lane quadrant per warp");
 };
 
@@ -455,6 +459,9 @@ __device__ __forceinline__ int paired_bfly(int tl, int q) {
 // twiddle + DFT of this thread's B = P / R butterflies (slots q + r * B)
 template <int LOGM, int P, bool INV, int NSL, int R, bool PAIRED, bool HALF>
 __device__ __forceinline__ void pstage_compute(double2 (&v)[P], int tl, const double2 (&w1s)[P]) {
+#ifdef FDE_EXP_NOFFT
+  return;
+#endif
   constexpr int B = P / R, NS = 1 << NSL;
 #pragma unroll
   for (int q = 0; q < B; ++q) {
@@ -489,17 +496,29 @@ __device__ __forceinline__ void pstage_twiddles(double2 (&w1s)[P], int tl, const
 }
 
 // Stockham write of a finished stage (NSL, R) to plane (re, im)
-template <int LOGM, int P, int NSL, int R, bool PAIRED>
+// Exchange-buffer swizzle p ^ ((p >> K) & 15) (K = 0: none).  Each exchange
+// picks the K that makes both its write and its read pattern free of 8-byte
+// bank conflicts (the paired stage's (j, NS - j) accesses need their own).
+template <int K>
+__device__ __forceinline__ int swzk(int p) {
+  if constexpr (K == 0) return p;
+  else return p ^ ((p >> K) & 15);
+}
+
+template <int LOGM, int P, int NSL, int R, bool PAIRED, int K>
 __device__ __forceinline__ void pstage_write(const double2 (&v)[P], double* re, double* im,
                                              int tl) {
-  constexpr int T = (1 << LOGM) / P, B = P / R, NS = 1 << NSL, SH = Log2<P>::v;
+#ifdef FDE_EXP_NOXCHG
+  return;
+#endif
+  constexpr int T = (1 << LOGM) / P, B = P / R, NS = 1 << NSL;
 #pragma unroll
   for (int q = 0; q < B; ++q) {
     const int j = PAIRED ? paired_bfly<B, T>(tl, q) : tl + q * T;
     const int base = ((j >> NSL) << (NSL + Log2<R>::v)) + (j & (NS - 1));
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const int p = swz<SH>(base + r * NS);
+      const int p = swzk<K>(base + r * NS);
       re[p] = v[q + r * B].x;
       im[p] = v[q + r * B].y;
     }
@@ -507,16 +526,19 @@ __device__ __forceinline__ void pstage_write(const double2 (&v)[P], double* re, 
 }
 
 // inputs of stage (R, PAIRED): butterfly j reads j + r * M / R
-template <int LOGM, int P, int R, bool PAIRED>
+template <int LOGM, int P, int R, bool PAIRED, int K>
 __device__ __forceinline__ void pstage_read(double2 (&v)[P], const double* re, const double* im,
                                             int tl) {
-  constexpr int M = 1 << LOGM, T = M / P, B = P / R, SH = Log2<P>::v;
+#ifdef FDE_EXP_NOXCHG
+  return;
+#endif
+  constexpr int M = 1 << LOGM, T = M / P, B = P / R;
 #pragma unroll
   for (int q = 0; q < B; ++q) {
     const int j = PAIRED ? paired_bfly<B, T>(tl, q) : tl + q * T;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const int p = swz<SH>(j + r * (M / R));
+      const int p = swzk<K>(j + r * (M / R));
       v[q + r * B] = make_double2(re[p], im[p]);
     }
   }
@@ -534,19 +556,20 @@ struct PFwd {
     pstage_compute<LOGM, P, false, NSL, P, false, HALF>(v, tl, w1s);
     double* re = buf + cur * 2 * S::BUF;
     if constexpr (S::NBUF == 1) __syncthreads();
-    pstage_write<LOGM, P, NSL, P, false>(v, re, re + S::BUF, tl);
     constexpr int NX = NSL + LP;
     constexpr bool LASTP = (LOGM - NX) < LP;  // next stage is the paired R0 stage
+    constexpr int K = LASTP ? S::KPF : S::KX;
+    pstage_write<LOGM, P, NSL, P, false, K>(v, re, re + S::BUF, tl);
     if constexpr (LASTP) {
       pstage_twiddles<LOGM, P, NX, S::R0, true>(w1s, tl, twM);
       __syncthreads();
-      pstage_read<LOGM, P, S::R0, true>(v, re, re + S::BUF, tl);
+      pstage_read<LOGM, P, S::R0, true, K>(v, re, re + S::BUF, tl);
       cur ^= S::NBUF - 1;
       pstage_compute<LOGM, P, false, NX, S::R0, true, false>(v, tl, w1s);
     } else {
       pstage_twiddles<LOGM, P, NX, P, false>(w1s, tl, twM);
       __syncthreads();
-      pstage_read<LOGM, P, P, false>(v, re, re + S::BUF, tl);
+      pstage_read<LOGM, P, P, false, K>(v, re, re + S::BUF, tl);
       cur ^= S::NBUF - 1;
       PFwd<LOGM, P, NX, false>::run(v, buf, cur, tl, twM, w1s);
     }
@@ -554,40 +577,47 @@ struct PFwd {
 };
 
 // Inverse radix-P stages from NSL (inputs in v); the last stays in registers.
+// hook(): called once the last stage's inputs are in registers (the exchange
+// buffer is then free for the epilogue operands, see fft_line_kernel_paired)
 template <int LOGM, int P, int NSL>
 struct PInvTail {
+  template <class Hook>
   __device__ __forceinline__ static void run(double2 (&v)[P], double* buf, int& cur, int tl,
-                                             const double2* twM, double2 (&w1s)[P]) {
+                                             const double2* twM, double2 (&w1s)[P],
+                                             const Hook& hook) {
     using S = PairedShape<LOGM, P>;
     constexpr int LP = S::LP;
     pstage_compute<LOGM, P, true, NSL, P, false, false>(v, tl, w1s);
     if constexpr (NSL + LP < LOGM) {
       double* re = buf + cur * 2 * S::BUF;
       if constexpr (S::NBUF == 1) __syncthreads();
-      pstage_write<LOGM, P, NSL, P, false>(v, re, re + S::BUF, tl);
+      pstage_write<LOGM, P, NSL, P, false, S::KX>(v, re, re + S::BUF, tl);
       pstage_twiddles<LOGM, P, NSL + LP, P, false>(w1s, tl, twM);
       __syncthreads();
-      pstage_read<LOGM, P, P, false>(v, re, re + S::BUF, tl);
+      pstage_read<LOGM, P, P, false, S::KX>(v, re, re + S::BUF, tl);
       cur ^= S::NBUF - 1;
-      PInvTail<LOGM, P, NSL + LP>::run(v, buf, cur, tl, twM, w1s);
+      if constexpr (NSL + 2 * LP >= LOGM) hook();
+      PInvTail<LOGM, P, NSL + LP>::run(v, buf, cur, tl, twM, w1s, hook);
     }
   }
 };
 
 // Full inverse: paired R0 stage (NS = 1) on the spectral slots, then radix P.
-template <int LOGM, int P>
+template <int LOGM, int P, class Hook>
 __device__ __forceinline__ void pinverse(double2 (&v)[P], double* buf, int& cur, int tl,
-                                         const double2* twM, double2 (&w1s)[P]) {
+                                         const double2* twM, double2 (&w1s)[P],
+                                         const Hook& hook) {
   using S = PairedShape<LOGM, P>;
   pstage_compute<LOGM, P, true, 0, S::R0, true, false>(v, tl, w1s);
   double* re = buf + cur * 2 * S::BUF;
   if constexpr (S::NBUF == 1) __syncthreads();
-  pstage_write<LOGM, P, 0, S::R0, true>(v, re, re + S::BUF, tl);
+  pstage_write<LOGM, P, 0, S::R0, true, S::KPI>(v, re, re + S::BUF, tl);
   pstage_twiddles<LOGM, P, S::REM, P, false>(w1s, tl, twM);
   __syncthreads();
-  pstage_read<LOGM, P, P, false>(v, re, re + S::BUF, tl);
+  pstage_read<LOGM, P, P, false, S::KPI>(v, re, re + S::BUF, tl);
   cur ^= S::NBUF - 1;
-  PInvTail<LOGM, P, S::REM>::run(v, buf, cur, tl, twM, w1s);
+  if constexpr (S::REM + S::LP >= LOGM) hook();
+  PInvTail<LOGM, P, S::REM>::run(v, buf, cur, tl, twM, w1s, hook);
 }
 
 // spectral partner slot of slot s = q + r * B0 (tl != 0 / tl == 0)
@@ -631,6 +661,12 @@ struct LineIO<YPass, EPI> {
   __device__ __forceinline__ double load(int d) const {
     return XT ? x[d] : x[(size_t)d * n1];
   }
+  __device__ __forceinline__ const double* xaddr(int d) const {
+    return XT ? x + d : x + (size_t)d * n1;
+  }
+  // the two operand streams staged through shared memory, and the rest
+  __device__ __forceinline__ const double* staged(int k, int d) const { return (k ? em : ep) + d; }
+  __device__ __forceinline__ Ops fetch_rest(int, double s0, double s1) const { return Ops{s0, s1}; }
   __device__ __forceinline__ Ops fetch(int d) const { return Ops{ep[d], em[d]}; }
   __device__ __forceinline__ void finish(int d, double ty, double tt, const Ops& o) const {
     const double v = c * (o.ep * ty + o.em * tt);
@@ -666,6 +702,18 @@ struct LineIO<XPass, EPI> {
     s2 = EPI == EPI_RHS ? p.src_scale : p.omega;
   }
   __device__ __forceinline__ double load(int d) const { return x[d]; }
+  __device__ __forceinline__ const double* xaddr(int d) const { return x + d; }
+  __device__ __forceinline__ const double* staged(int k, int d) const { return (k ? dm : dp) + d; }
+  __device__ __forceinline__ Ops fetch_rest(int d, double s0, double s1) const {
+    Ops o;
+    o.x = x[d];
+    o.dp = s0;
+    o.dm = s1;
+    o.q = q ? q[d] : 0.0;
+    o.e1 = EPI == EPI_STORE ? 0.0 : e1[d];
+    o.e2 = EPI == EPI_JACOBI ? e2[d] : 0.0;
+    return o;
+  }
   __device__ __forceinline__ Ops fetch(int d) const {
     Ops o;
     o.x = x[d];
@@ -695,142 +743,186 @@ __global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THRE
     fft_line_kernel_paired(const Pol p) {
   constexpr int P = LOGM >= 11 ? 16 : 8;
   using S = PairedShape<LOGM, P>;
+  using IO = LineIO<Pol, EPI>;
   constexpr int T = S::T, H = P / 2, R0 = S::R0, B0 = S::B0, NS0 = S::NS0;
   extern __shared__ __align__(16) double smem[];
+  double* const xbuf = smem + S::NBUF * 2 * S::BUF;  // next line's input (own slots only)
   __shared__ uint32_t s_tbase;
   const int tl = threadIdx.x, warp = tl >> 5;
-  const int line = blockIdx.x;
-  const int n = p.blk.n;
+  const int n = p.blk.n, nl = p.nlines();
 
-  if (warp == 0) tmem_alloc<S::TCOLS>(&s_tbase);
-#if FDE_L2_PREFETCH
-  for (int c = tl; c * 16 < n; c += T) p.prefetch(line, c);
-#endif
-
-  // 1) z_m = x_2m + i x_2m+1, m = tl + s*T; zero padded (n <= M: s < P/2 only).
-  //    Slot s needs guards only when its last thread's positions reach n.
-  const LineIO<Pol, EPI> io(p, line, 2 * tl);
-  double2 v[P];
-#pragma unroll
-  for (int s = 0; s < H; ++s) {
-    const int i0 = 2 * (tl + s * T), d = 2 * s * T;
+  // Persistent CTA: lines blockIdx.x, + gridDim.x, ...  Each thread copies the
+  // next line's input slots (its own positions) into xbuf while the current
+  // line is transformed, so only the first line waits for HBM.
+  auto prefetch_x = [&](int line) {
 #ifdef FDE_EXP_NOX
-    v[s].x = 1.0 / (i0 + 1);
-    v[s].y = 1.0 / (i0 + 2);
-#else
-    if (2 * T * (s + 1) <= n) {
-      v[s].x = io.load(d);
-      v[s].y = io.load(d + 1);
-    } else {
-      v[s].x = i0 < n ? io.load(d) : 0.0;
-      v[s].y = i0 + 1 < n ? io.load(d + 1) : 0.0;
-    }
+    return;
 #endif
-    v[s + H] = make_double2(0.0, 0.0);
+    const IO io(p, line, 2 * tl);
+#pragma unroll
+    for (int s = 0; s < H; ++s) {
+      const int i0 = 2 * (tl + s * T), d = 2 * s * T;
+      cp_async8(xbuf + i0, io.xaddr(i0 < n ? d : 0), i0 < n ? 8 : 0);
+      cp_async8(xbuf + i0 + 1, io.xaddr(i0 + 1 < n ? d + 1 : 0), i0 + 1 < n ? 8 : 0);
+    }
+    cp_async_commit();
+  };
+#ifdef FDE_EXP_STAGGER
+  {
+    const int slot = blockIdx.x / 148;
+    for (int k = 0; k < slot; ++k) __nanosleep(FDE_EXP_STAGGER);
   }
+#endif
+  if (warp == 0) tmem_alloc<S::TCOLS>(&s_tbase);
+  if (blockIdx.x < nl) prefetch_x(blockIdx.x);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   const uint32_t tq = s_tbase + ((uint32_t)(warp * 32) << 16);  // this warp's lane quadrant
   const uint32_t tqy = tq, tqt = tq + 4 * P;                    // Qy, Qt column ranges
+  const double* const ep0 = smem;            // staged epilogue operands (exchange buffer)
+  const double* const ep1 = smem + S::BUF;
 
-  // 2) forward transform; ends with this thread's paired slots in v
-  double2 w1s[P];
-  int cur = 0;
-  PFwd<LOGM, P, 0, true>::run(v, smem, cur, tl, p.blk.twM, w1s);
-
-  // 3) spectral step (see fft_line_kernel): partners are in registers; results
-  //    go to tensor memory in groups of 4 slots
-  {
-    const bool t0 = tl == 0;
-    const double2* abv = reinterpret_cast<const double2*>(p.blk.ab);
-#pragma unroll
-    for (int g = 0; g < P; g += 4) {
-      double2 qy[4], qt[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int s = g + c, q = s % B0, r = s / B0;
-        const int k = paired_bfly<B0, T>(tl, q) + r * NS0;
-        constexpr int dummy = 0;
-        (void)dummy;
-        const double2 z = v[s];
-        const double2 zm0 = v[partner_slot<B0, R0>(s, true)];
-        const double2 zm1 = v[partner_slot<B0, R0>(s, false)];
-        const double mr = t0 ? zm0.x : zm1.x, mi = t0 ? zm0.y : zm1.y;
-#ifdef FDE_EXP_NOAB
-        const double2 ca = make_double2(1.0 + k, 0.5), cb = make_double2(0.25, 0.125 * k);
-#else
-        const double2 ca = __ldg(abv + k), cb = __ldg(abv + S::M + k);
-#endif
-        const double t1 = ca.x * z.x, t2 = ca.y * z.y, t3 = ca.x * z.y, t4 = ca.y * z.x;
-        const double u1 = cb.x * mr, u2 = cb.y * mi, u3 = cb.y * mr, u4 = cb.x * mi;
-        qy[c] = make_double2((t1 - t2) + (u1 + u2), (t3 + t4) + (u3 - u4));
-        qt[c] = make_double2((t1 + t2) + (u2 - u1), (t3 - t4) + (u3 + u4));
-      }
-      tmem_st4(tqy + 4 * g, qy);
-      tmem_st4(tqt + 4 * g, qt);
-    }
-  }
-  tmem_wait_st();
-
-  // 4) inverse of Qy -> T x (packed; its H output slots are parked in the Qy
-  //    columns), then 5) inverse of Qt -> T^T x.  One copy of the inverse code
-  //    (instruction-cache footprint): both start on exchange buffer 0.
-  const int n_inv = 2 + (n < 0);  // opaque trip count: ptxas keeps the loop rolled
 #pragma unroll 1
-  for (int it = 0; it < n_inv; ++it) {
-    const uint32_t src = it ? tqt : tqy;
-#pragma unroll
-    for (int g = 0; g < P; g += 4) {
-      double2 t[4];
-      tmem_ld4(src + 4 * g, t);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) v[g + c] = t[c];
-    }
-    cur = 0;
-    pinverse<LOGM, P>(v, smem, cur, tl, p.blk.twM, w1s);
-    if (it == 0) {
-#pragma unroll
-      for (int g = 0; g < H; g += 4) {
-        double2 t[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) t[c] = v[g + c];
-        tmem_st4(tqy + 4 * g, t);
-      }
-      tmem_wait_st();
-    }
-  }
-
-  // 6) epilogue in groups of 4 slots (8 positions)
-#pragma unroll
-  for (int g = 0; g < H; g += 4) {
-    double2 ty[4];
-    tmem_ld4(tqy + 4 * g, ty);
-    typename LineIO<Pol, EPI>::Ops o[8];
-    if (2 * T * (g + 4) <= n) {  // whole group in range for every thread (uniform)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int d = 2 * (g + c) * T;
-#ifdef FDE_EXP_NOEPI
-        o[2 * c] = typename LineIO<Pol, EPI>::Ops{};
-        o[2 * c + 1] = typename LineIO<Pol, EPI>::Ops{};
-#else
-        o[2 * c] = io.fetch(d);
-        o[2 * c + 1] = io.fetch(d + 1);
+  for (int line = blockIdx.x; line < nl; line += gridDim.x) {
+    const IO io(p, line, 2 * tl);
+#if FDE_L2_PREFETCH
+    for (int c = tl; c * 16 < n; c += T) p.prefetch(line, c);
 #endif
-      }
+    // 1) z_m = x_2m + i x_2m+1, m = tl + s*T, from this thread's xbuf slots
+    //    (zero filled beyond n); then start the next line's copy
+    cp_async_wait_all();
+    double2 v[P];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int d = 2 * (g + c) * T;
-        io.finish(d, ty[c].x, v[g + c].x, o[2 * c]);
-        io.finish(d + 1, ty[c].y, v[g + c].y, o[2 * c + 1]);
-      }
-    } else {
+    for (int s = 0; s < H; ++s) {
+      const double2 t = *reinterpret_cast<const double2*>(xbuf + 2 * (tl + s * T));
+      v[s] = t;
+      v[s + H] = make_double2(0.0, 0.0);
+    }
+    if (line + (int)gridDim.x < nl) prefetch_x(line + gridDim.x);
+
+    // 2) forward transform; ends with this thread's paired slots in v
+    double2 w1s[P];
+    int cur = 0;
+    PFwd<LOGM, P, 0, true>::run(v, smem, cur, tl, p.blk.twM, w1s);
+
+    // 3) spectral step (see fft_line_kernel): partners are in registers;
+    //    results go to tensor memory in groups of 4 slots
+    {
+      const bool t0 = tl == 0;
+      const double2* abv = reinterpret_cast<const double2*>(p.blk.ab);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
-        if (i0 < n) io.finish(d, ty[c].x, v[g + c].x, io.fetch(d));
-        if (i0 + 1 < n) io.finish(d + 1, ty[c].y, v[g + c].y, io.fetch(d + 1));
+      for (int g = 0; g < P; g += 4) {
+        double2 qy[4], qt[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int s = g + c, q = s % B0, r = s / B0;
+          const int k = paired_bfly<B0, T>(tl, q) + r * NS0;
+          const double2 z = v[s];
+          const double2 zm0 = v[partner_slot<B0, R0>(s, true)];
+          const double2 zm1 = v[partner_slot<B0, R0>(s, false)];
+          const double mr = t0 ? zm0.x : zm1.x, mi = t0 ? zm0.y : zm1.y;
+#ifdef FDE_EXP_NOAB
+          const double2 ca = make_double2(1.0 + k, 0.5), cb = make_double2(0.25, 0.125 * k);
+#else
+          const double2 ca = __ldg(abv + k), cb = __ldg(abv + S::M + k);
+#endif
+          const double t1 = ca.x * z.x, t2 = ca.y * z.y, t3 = ca.x * z.y, t4 = ca.y * z.x;
+          const double u1 = cb.x * mr, u2 = cb.y * mi, u3 = cb.y * mr, u4 = cb.x * mi;
+          qy[c] = make_double2((t1 - t2) + (u1 + u2), (t3 + t4) + (u3 - u4));
+          qt[c] = make_double2((t1 + t2) + (u2 - u1), (t3 - t4) + (u3 + u4));
+        }
+        tmem_st4(tqy + 4 * g, qy);
+        tmem_st4(tqt + 4 * g, qt);
+      }
+    }
+    tmem_wait_st();
+
+    // 4) inverse of Qy -> T x (packed; its H output slots are parked in the Qy
+    //    columns), then 5) inverse of Qt -> T^T x.  One copy of the inverse
+    //    code (instruction-cache footprint); both start on exchange buffer 0.
+    //    Once the second inverse's last stage has its inputs in registers, the
+    //    exchange buffer receives two epilogue operand streams (cp.async),
+    //    overlapped with that stage's butterflies.
+    const int n_inv = 2 + (n < 0);  // opaque trip count: ptxas keeps the loop rolled
+#pragma unroll 1
+    for (int it = 0; it < n_inv; ++it) {
+      const uint32_t src = it ? tqt : tqy;
+#pragma unroll
+      for (int g = 0; g < P; g += 4) {
+        double2 t[4];
+        tmem_ld4(src + 4 * g, t);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[g + c] = t[c];
+      }
+      cur = 0;
+      auto stage_epilogue = [&]() {
+        if (it == 0) return;
+#ifdef FDE_EXP_NOEPI
+        return;
+#endif
+        __syncthreads();  // every thread has read its last-stage inputs
+#pragma unroll
+        for (int s = 0; s < H; ++s) {
+          const int i0 = 2 * (tl + s * T), d = 2 * s * T;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool ok = i0 + e < n;
+            cp_async8(smem + i0 + e, io.staged(0, ok ? d + e : 0), ok ? 8 : 0);
+            cp_async8(smem + S::BUF + i0 + e, io.staged(1, ok ? d + e : 0), ok ? 8 : 0);
+          }
+        }
+        cp_async_commit();
+      };
+      pinverse<LOGM, P>(v, smem, cur, tl, p.blk.twM, w1s, stage_epilogue);
+      if (it == 0) {
+#pragma unroll
+        for (int g = 0; g < H; g += 4) {
+          double2 t[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) t[c] = v[g + c];
+          tmem_st4(tqy + 4 * g, t);
+        }
+        tmem_wait_st();
+      }
+    }
+
+    // 6) epilogue in groups of 4 slots (8 positions); own staged slots only
+    cp_async_wait_all();
+#pragma unroll
+    for (int g = 0; g < H; g += 4) {
+      double2 ty[4];
+      tmem_ld4(tqy + 4 * g, ty);
+      typename IO::Ops o[8];
+      if (2 * T * (g + 4) <= n) {  // whole group in range for every thread (uniform)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
+          const double2 a = *reinterpret_cast<const double2*>(ep0 + i0);
+          const double2 b = *reinterpret_cast<const double2*>(ep1 + i0);
+#ifdef FDE_EXP_NOEPI
+          o[2 * c] = typename IO::Ops{a.x, b.x};
+          o[2 * c + 1] = typename IO::Ops{a.y, b.y};
+#else
+          o[2 * c] = io.fetch_rest(d, a.x, b.x);
+          o[2 * c + 1] = io.fetch_rest(d + 1, a.y, b.y);
+#endif
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int d = 2 * (g + c) * T;
+          io.finish(d, ty[c].x, v[g + c].x, o[2 * c]);
+          io.finish(d + 1, ty[c].y, v[g + c].y, o[2 * c + 1]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
+          if (i0 < n)
+            io.finish(d, ty[c].x, v[g + c].x, io.fetch_rest(d, ep0[i0], ep1[i0]));
+          if (i0 + 1 < n)
+            io.finish(d + 1, ty[c].y, v[g + c].y, io.fetch_rest(d + 1, ep0[i0 + 1], ep1[i0 + 1]));
+        }
       }
     }
   }
@@ -977,9 +1069,35 @@ void launch_paired_epi(const P& p, cudaStream_t s) {
   if (!configured) {
     FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+    // resident CTAs are register-bound; give shared memory the whole carveout
+    FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
+                                  cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  (int)cudaSharedmemCarveoutMaxShared));
     configured = true;
   }
-  fft_line_kernel_paired<LOGM, P, EPI><<<lines_of(p), S::THREADS, S::SMEM, s>>>(p);
+  static int max_ctas = 0;  // resident CTAs on the device (persistent grid)
+  if (!max_ctas) {
+    // registers, shared memory and tensor-memory columns per SM, whichever
+    // binds (the occupancy API does not see the TMEM allocation)
+    int dev = 0, sms = 0, smem_sm = 0, smem_rsv = 0, regs_sm = 0;
+    FDE_CUDA(cudaGetDevice(&dev));
+    FDE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FDE_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+    FDE_CUDA(cudaDeviceGetAttribute(&smem_rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev));
+    FDE_CUDA(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
+    cudaFuncAttributes fa{};
+    FDE_CUDA(cudaFuncGetAttributes(&fa, fft_line_kernel_paired<LOGM, P, EPI>));
+    const int regs_cta = ((fa.numRegs * 32 + 255) / 256 * 256) * (S::THREADS / 32);
+    int per_sm = regs_sm / regs_cta;
+    const int by_smem = smem_sm / (int)(S::SMEM + fa.sharedSizeBytes + smem_rsv);
+    const int by_tmem = 512 / S::TCOLS;
+    per_sm = per_sm < by_smem ? per_sm : by_smem;
+    per_sm = per_sm < by_tmem ? per_sm : by_tmem;
+    max_ctas = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const int lines = lines_of(p);
+  fft_line_kernel_paired<LOGM, P, EPI><<<lines < max_ctas ? lines : max_ctas, S::THREADS,
+                                         S::SMEM, s>>>(p);
   FDE_LAUNCH_CHECK();
 }
 

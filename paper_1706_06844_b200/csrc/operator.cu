@@ -341,7 +341,18 @@ void StructuredOp::run_impl(const InMap* in, const double* x, double* out, doubl
   yp.emT = d_emT_.get();
   yp.c = sign * s_over_r_;
   yp.q = d_q_.get();
+#ifdef FDE_EXP_QTX
+  if (yp.xT) {  // column pass writes Q transposed in place of its input, then one transpose
+    yp.q = d_xT_.get();
+    yp.qT = 1;
+    launch_line_pass(yp, s);
+    launch_transpose(d_xT_.get(), d_q_.get(), (int)n2_, (int)n1_, s);
+  } else {
+    launch_line_pass(yp, s);
+  }
+#else
   launch_line_pass(yp, s);
+#endif
   XPass xp{};
   xp.blk = ax_.dev();
   xp.n1 = (int)n1_;

@@ -71,3 +71,19 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, double2 (&v)[4]) {
 }
 
 }  // namespace fde_b200
+
+namespace fde_b200 {
+// ---- cp.async (LDGSTS) helpers: global -> shared without registers --------
+// 8-byte copy; src_bytes = 0 zero-fills the destination (address must still be valid)
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_addr_u32(smem_dst)),
+               "l"(gsrc), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+}  // namespace fde_b200

@@ -211,7 +211,8 @@ int fde_march_create(const fde_problem* p, size_t n1, size_t n2, size_t steps,
  * from zero, u <- solution.  source: v(x_i, y_j, t^{m-1/2}) as
  *   source_mode 0: evaluated by the library (problem callback or preset),
  *   source_mode 1: HOST array (copied to the device inside the call),
- *   source_mode 2: DEVICE array. */
+ *   source_mode 2: DEVICE array,
+ *   source_mode 3: the array given to fde_march_prefetch_source. */
 int fde_march_step(fde_march h, const double* source, int source_mode, void* stream,
                    size_t* iterations, double* residual);
 /* Current step index m (steps taken so far) */
@@ -220,6 +221,19 @@ int fde_march_steps_taken(fde_march h, size_t* m);
 int fde_march_solution(fde_march h, double* u, int to_host, void* stream);
 /* Device pointer of u^m (valid until the next step) */
 int fde_march_solution_ptr(fde_march h, const double** u_dev);
+/* Pipelined host I/O (no reference counterpart: time_march keeps everything
+ * on the host, driver.cpp:10-69).  The copies run on the march's own copy
+ * stream, overlapped with the neighbouring steps' solves:
+ *   fde_march_prefetch_source: H2D of a coming step's source from a host
+ *     (preferably pinned) array, at most two ahead; each fde_march_step with
+ *     source_mode 3 consumes the oldest one.
+ *   fde_march_solution_async: D2H of u^m into a host array; the data is valid
+ *     after fde_march_wait.  The step that would overwrite u^m's buffer (two
+ *     steps later) waits for this copy on the device.
+ *   fde_march_wait: block until every copy issued so far has completed. */
+int fde_march_prefetch_source(fde_march h, const double* host_source);
+int fde_march_solution_async(fde_march h, double* host_u);
+int fde_march_wait(fde_march h);
 int fde_march_destroy(fde_march h);
 
 /* time_march (proj/include/fde/driver.hpp:39-40): all steps, host outputs.

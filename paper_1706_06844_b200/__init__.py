@@ -131,6 +131,9 @@ _SIGS = {
     "fde_march_steps_taken": (_c_int, [_c_vp, ctypes.POINTER(_c_size)]),
     "fde_march_solution": (_c_int, [_c_vp, _c_vp, _c_int, _c_vp]),
     "fde_march_solution_ptr": (_c_int, [_c_vp, ctypes.POINTER(_c_vp)]),
+    "fde_march_prefetch_source": (_c_int, [_c_vp, _c_vp]),
+    "fde_march_solution_async": (_c_int, [_c_vp, _c_vp]),
+    "fde_march_wait": (_c_int, [_c_vp]),
     "fde_march_destroy": (_c_int, [_c_vp]),
     "fde_time_march": (_c_int, [ctypes.POINTER(_FdeProblem), _c_size, _c_size, _c_size,
                                 ctypes.POINTER(_DriverConfig), _P, ctypes.POINTER(_c_size), _P, _P]),
@@ -596,12 +599,17 @@ class March:
         _check(load_library().fde_march_create(ctypes.byref(self._s), n1, n2, steps,
                                                ctypes.byref(self._cfg), ctypes.byref(self._h)))
 
+    PREFETCHED = "prefetched"
+
     def step(self, source=None, stream=None):
         """Advance one step.  source: None (library evaluates it), a numpy host
-        array (copied H2D inside the call) or a CUDA tensor (used in place)."""
+        array (copied H2D inside the call), a CUDA tensor (used in place) or
+        March.PREFETCHED (the array given to prefetch_source)."""
         it, res = _c_size(), _c_dbl()
         if source is None:
             ptr, mode = None, 0
+        elif isinstance(source, str) and source == March.PREFETCHED:
+            ptr, mode = None, 3
         elif isinstance(source, np.ndarray):
             ptr, mode = source.ctypes.data, 1
         else:
@@ -615,6 +623,19 @@ class March:
             out = np.zeros(self.n1 * self.n2)
         _check(load_library().fde_march_solution(self._h, out.ctypes.data, 1, _stream(stream)))
         return out
+
+    def prefetch_source(self, host_source: np.ndarray) -> None:
+        """Start the H2D copy of a coming step's source, at most two ahead
+        (keep the array alive until that step; pinned memory makes the copy
+        asynchronous).  step(March.PREFETCHED) consumes the oldest."""
+        _check(load_library().fde_march_prefetch_source(self._h, host_source.ctypes.data))
+
+    def solution_async(self, out: np.ndarray) -> None:
+        """Start the D2H copy of u^m into `out` (valid after wait())."""
+        _check(load_library().fde_march_solution_async(self._h, out.ctypes.data))
+
+    def wait(self) -> None:
+        _check(load_library().fde_march_wait(self._h))
 
     def solution_device_ptr(self) -> int:
         p = _c_vp()

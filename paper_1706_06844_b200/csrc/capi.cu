@@ -43,6 +43,40 @@ struct fde_march_s {
   std::vector<double> host_src;
   double scale = 0.0;  // 2 hx^alpha (problem.cpp:82)
   size_t m = 0;
+  // pipelined host I/O (fde_march_prefetch_source / _solution_async)
+  cudaStream_t cs = nullptr;            // copy stream
+  cudaEvent_t ev_step = nullptr;        // u^m final on the compute stream
+  cudaEvent_t ev_d2h = nullptr;         // last D2H of a solution buffer done
+  const double* d2h_buf = nullptr;      // the buffer that D2H reads
+  // prefetched sources: a ring of three device buffers, up to two in flight
+  DevBuf<double> ring[3];
+  cudaEvent_t ev_ready[3] = {};  // H2D into ring[i] done (copy stream)
+  cudaEvent_t ev_free[3] = {};   // the rhs assembly that read ring[i] done (compute stream)
+  int pending[2] = {-1, -1};     // FIFO of filled ring slots
+  int npending = 0;
+  int cur_src = -1;
+  void ensure_io() {
+    if (cs) return;
+    FDE_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    FDE_CUDA(cudaEventCreateWithFlags(&ev_step, cudaEventDisableTiming));
+    FDE_CUDA(cudaEventCreateWithFlags(&ev_d2h, cudaEventDisableTiming));
+    for (int i = 0; i < 3; ++i) {
+      FDE_CUDA(cudaEventCreateWithFlags(&ev_ready[i], cudaEventDisableTiming));
+      FDE_CUDA(cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming));
+    }
+  }
+  ~fde_march_s() {
+    if (cs) {
+      cudaStreamSynchronize(cs);
+      cudaStreamDestroy(cs);
+      cudaEventDestroy(ev_step);
+      cudaEventDestroy(ev_d2h);
+      for (int i = 0; i < 3; ++i) {
+        cudaEventDestroy(ev_ready[i]);
+        cudaEventDestroy(ev_free[i]);
+      }
+    }
+  }
 };
 
 namespace {
@@ -579,14 +613,25 @@ int fde_march_step(fde_march h, const double* source, int source_mode, void* str
     } else if (source_mode == 2) {
       need(source != nullptr, "null source");
       src = source;
+    } else if (source_mode == 3) {
+      need(h->npending > 0, "no prefetched source (fde_march_prefetch_source)");
+      const int b = h->pending[0];
+      h->pending[0] = h->pending[1];
+      --h->npending;
+      FDE_CUDA(cudaStreamWaitEvent(s, h->ev_ready[b], 0));
+      src = h->ring[b].get();
+      h->cur_src = b;
     } else {
-      throw InvalidArgument("source_mode must be 0, 1 or 2");
+      throw InvalidArgument("source_mode must be 0, 1, 2 or 3");
     }
+    // the solve overwrites h->x: a pending D2H of that buffer must finish first
+    if (h->cs && h->d2h_buf == h->x.get()) FDE_CUDA(cudaStreamWaitEvent(s, h->ev_d2h, 0));
     // assemble_rhs (problem.cpp:73-89): b = apply_rhs(u) + 2 hx^alpha v, fused
     EpiArgs e;
     e.src = src;
     e.src_scale = h->scale;
     h->op->run(h->u.get(), h->b.get(), -1.0, EPI_RHS, e, s);
+    if (source_mode == 3) FDE_CUDA(cudaEventRecord(h->ev_free[h->cur_src], s));
     SolverConfig c{h->cfg.tol, h->cfg.restart, h->cfg.max_outer};
     const Precond* pc = h->pc->kind() == PC_NONE ? nullptr : h->pc.get();
     const StructuredOp& a = h->p.time_dependent_coeffs ? *h->next : *h->op;
@@ -595,6 +640,8 @@ int fde_march_step(fde_march h, const double* source, int source_mode, void* str
                                : h->ws->gmres(a, pc, c, h->b.get(), h->x.get(), s);
     std::swap(h->u, h->x);
     if (h->p.time_dependent_coeffs) std::swap(h->op, h->next);  // driver.cpp:51
+    h->ensure_io();
+    FDE_CUDA(cudaEventRecord(h->ev_step, s));  // u^m final; orders the copy stream
     h->m = m;
     if (iterations) *iterations = r.total_iterations;
     if (residual) *residual = r.residual_history.back();
@@ -615,6 +662,45 @@ int fde_march_solution(fde_march h, double* u, int to_host, void* stream) {
     FDE_CUDA(cudaMemcpyAsync(u, h->u.get(), h->g.size() * sizeof(double),
                              to_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
     if (to_host) FDE_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int fde_march_prefetch_source(fde_march h, const double* host_source) {
+  return guard([&] {
+    need(h && host_source, "null argument");
+    need(h->npending < 2, "two prefetched sources are already pending");
+    h->ensure_io();
+    const size_t n = h->g.size();
+    int b = 0;  // a ring slot that is neither pending nor the last one consumed
+    while (b == h->cur_src || (h->npending > 0 && h->pending[0] == b) ||
+           (h->npending > 1 && h->pending[1] == b))
+      ++b;
+    if (h->ring[b].size() != n) h->ring[b].alloc(n);
+    // the slot last fed an earlier step's rhs assembly: order after it
+    FDE_CUDA(cudaStreamWaitEvent(h->cs, h->ev_free[b], 0));
+    FDE_CUDA(cudaMemcpyAsync(h->ring[b].get(), host_source, n * sizeof(double),
+                             cudaMemcpyHostToDevice, h->cs));
+    FDE_CUDA(cudaEventRecord(h->ev_ready[b], h->cs));
+    h->pending[h->npending++] = b;
+  });
+}
+
+int fde_march_solution_async(fde_march h, double* host_u) {
+  return guard([&] {
+    need(h && host_u, "null argument");
+    h->ensure_io();
+    FDE_CUDA(cudaStreamWaitEvent(h->cs, h->ev_step, 0));  // u^m written by the last step
+    FDE_CUDA(cudaMemcpyAsync(host_u, h->u.get(), h->g.size() * sizeof(double),
+                             cudaMemcpyDeviceToHost, h->cs));
+    FDE_CUDA(cudaEventRecord(h->ev_d2h, h->cs));
+    h->d2h_buf = h->u.get();
+  });
+}
+
+int fde_march_wait(fde_march h) {
+  return guard([&] {
+    need(h != nullptr, "null handle");
+    if (h->cs) FDE_CUDA(cudaStreamSynchronize(h->cs));
   });
 }
 

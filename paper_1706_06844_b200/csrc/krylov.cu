@@ -42,6 +42,32 @@ __global__ void k_bicg_x(size_t n, double alpha, double omg, const double* __res
        i += (size_t)gridDim.x * blockDim.x)
     x[i] += alpha * p[i] + omg * sv[i];
 }
+// Small scalar transfers between device scratch and the pinned host staging
+// (UVA-mapped): one tiny kernel instead of a DMA copy, so the solver's
+// per-iteration round trip never queues behind bulk host copies running on
+// other streams (the march's pipelined source / solution transfers).
+__global__ void k_copy_small(double* __restrict__ dst, const double* __restrict__ src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+void copy_small(double* dst, const double* src, size_t n, cudaStream_t s) {
+  k_copy_small<<<1, 128, 0, s>>>(dst, src, (int)n);
+  FDE_LAUNCH_CHECK();
+}
+
+// device-to-device vector copy on the SMs (a DMA copy would queue behind the
+// march's bulk host transfers on the copy engines)
+__global__ void k_copy(size_t n, const double* __restrict__ x, double* __restrict__ y) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    y[i] = x[i];
+}
+void copy_vec(size_t n, const double* x, double* y, cudaStream_t s) {
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_copy<<<blocks ? blocks : 1, 256, 0, s>>>(n, x, y);
+  FDE_LAUNCH_CHECK();
+}
+
 int nblocks(size_t n) {
   int b = (int)((n + 255) / 256);
   return b > 148 * 8 ? 148 * 8 : (b ? b : 1);
@@ -84,7 +110,7 @@ void Precond::record(const double* r, double* z, cudaStream_t s) const {
 
 void Precond::apply(const double* r, double* z, cudaStream_t s) const {
   if (kind_ == PC_NONE) {
-    FDE_CUDA(cudaMemcpyAsync(z, r, n_ * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    copy_vec(n_, r, z, s);
     return;
   }
   if (!use_graphs_) {
@@ -140,11 +166,11 @@ KrylovWorkspace::KrylovWorkspace(size_t n, size_t restart) : n_(n), rst_(restart
 void KrylovWorkspace::precondition(const Precond* m, const double* r, double* z,
                                    cudaStream_t s) {
   if (m) m->apply(r, z, s);
-  else FDE_CUDA(cudaMemcpyAsync(z, r, n_ * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  else copy_vec(n_, r, z, s);
 }
 
 void KrylovWorkspace::fetch(size_t count, cudaStream_t s) {
-  FDE_CUDA(cudaMemcpyAsync(hsc_, dsc_.get(), count * sizeof(double), cudaMemcpyDeviceToHost, s));
+  copy_small(hsc_, dsc_.get(), count, s);
   FDE_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -196,8 +222,7 @@ KrylovResult KrylovWorkspace::gmres(const StructuredOp& a, const Precond* m,
   double* const dreo = dsc_.get() + ld + 2;   // re-orthogonalisation coefficients
   auto lincomb_into = [&](const double* x0, double* out, const std::vector<double>& coef) {
     std::copy(coef.begin(), coef.end(), hsc_ + 4 * (rst_ + 2) + 16);
-    FDE_CUDA(cudaMemcpyAsync(dcoef_.get(), hsc_ + 4 * (rst_ + 2) + 16,
-                             coef.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    copy_small(dcoef_.get(), hsc_ + 4 * (rst_ + 2) + 16, coef.size(), s);
     vec_lincomb(n, x0, dptr_.get(), dcoef_.get(), (int)coef.size(), out, s);
     FDE_CUDA(cudaStreamSynchronize(s));  // the pinned staging slot is reused
   };
@@ -302,7 +327,7 @@ KrylovResult KrylovWorkspace::gmres(const StructuredOp& a, const Precond* m,
   if (res.residual_history.empty()) res.residual_history.push_back(final_rel);
   else res.residual_history.back() = final_rel;
   if (x != x_out)
-    FDE_CUDA(cudaMemcpyAsync(x_out, x, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    copy_vec(n, x, x_out, s);
   return res;
 }
 
@@ -328,7 +353,7 @@ KrylovResult KrylovWorkspace::bicgstab(const StructuredOp& a, const Precond* m,
     res.residual_history.push_back(0.0);
     return res;
   }
-  FDE_CUDA(cudaMemcpyAsync(rh, r, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  copy_vec(n, r, rh, s);
   res.residual_history.push_back(1.0);
   auto true_res = [&](const double* xv, double* out) {  // out = M^-1 (b - A xv)
     EpiArgs e;
@@ -342,7 +367,7 @@ KrylovResult KrylovWorkspace::bicgstab(const StructuredOp& a, const Precond* m,
     const double rho_new = dot_host(rh, r, s);
     if (rho_new == 0.0) break;
     if (it == 0) {
-      FDE_CUDA(cudaMemcpyAsync(p, r, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      copy_vec(n, r, p, s);
     } else {
       const double beta = (rho_new / rho) * (alpha / omg);
       k_bicg_p<<<nblocks(n), 256, 0, s>>>(n, beta, omg, r, v, p);
@@ -359,11 +384,11 @@ KrylovResult KrylovWorkspace::bicgstab(const StructuredOp& a, const Precond* m,
     const double srel = nrm2_host(sv, s) / norm_b;
     if (srel <= cfg.tol) {  // half step: verify x + alpha p
       double* trial = trial_.get();
-      FDE_CUDA(cudaMemcpyAsync(trial, x, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      copy_vec(n, x, trial, s);
       vec_axpy(n, alpha, p, trial, s);
       const double trel = true_res(trial, tv);
       if (trel <= cfg.tol) {
-        FDE_CUDA(cudaMemcpyAsync(x, trial, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        copy_vec(n, trial, x, s);
         res.residual_history.push_back(trel);
         res.converged = true;
         break;

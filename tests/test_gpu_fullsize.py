@@ -151,3 +151,29 @@ def test_bicgstab_cfg3_full(cuda, coarse):
     its, us = run_march(3, 1023, 16, mg_cfg(tol=1e-10, restart=30, coarse=coarse, solver=1))
     np.testing.assert_array_equal(its, gd["its"])
     assert compare_summary(us, gd, 1e-10) <= 1e-10
+
+
+def test_march_pipelined_host_io(cuda):
+    """prefetch_source / solution_async (pipelined host I/O) give the same
+    trajectory as plain host-array steps (cfg2 grid, 4 steps)."""
+    steps = 4
+    p = fde.Problem.preset_config(2, steps=steps)
+    n = p.n
+    srcs = [np.ascontiguousarray(p.sample_source(n, n, steps, m)) for m in range(1, steps + 1)]
+    ref = fde.March(p, n, n, steps, mg_cfg())
+    want = []
+    for m in range(steps):
+        ref.step(srcs[m])
+        want.append(ref.solution())
+    pipe = fde.March(p, n, n, steps, mg_cfg())
+    outs = [np.zeros(n * n) for _ in range(steps)]
+    pipe.prefetch_source(srcs[0])
+    pipe.prefetch_source(srcs[1])
+    for m in range(steps):
+        pipe.step(fde.March.PREFETCHED)
+        if m + 2 < steps:
+            pipe.prefetch_source(srcs[m + 2])
+        pipe.solution_async(outs[m])
+    pipe.wait()
+    for m in range(steps):
+        np.testing.assert_array_equal(outs[m], want[m])

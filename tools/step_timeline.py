@@ -1,0 +1,37 @@
+"""Kernel timeline of cfg4 time steps (CUPTI via torch.profiler): total span,
+sum of kernel durations, gaps, and the per-kernel-family totals."""
+import sys
+from collections import defaultdict
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_1706_06844_b200 as fde
+
+steps = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+p = fde.Problem.preset_config(4, steps=8)
+cfg = fde.DriverConfig(precond=fde.PRECOND_MGM, tol=1e-8, restart=20, max_outer=100, omega=0.7,
+                       cycles=1, coarse=fde.COARSE_SWEEPS, coarse_sweeps=3)
+m = fde.March(p, p.n, p.n, 8, cfg)
+for _ in range(2):
+    m.step()
+torch.cuda.synchronize()
+with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+    for _ in range(steps):
+        m.step()
+    torch.cuda.synchronize()
+ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+ks = sorted((e.time_range.start, e.time_range.end, e.name) for e in ev)
+span = ks[-1][1] - ks[0][0]
+busy = sum(b - a for a, b, _ in ks)
+gaps = [ks[i + 1][0] - ks[i][1] for i in range(len(ks) - 1)]
+print(f"{steps} steps: span {span / 1e3:.2f} ms, kernels {len(ks)}, busy {busy / 1e3:.2f} ms, "
+      f"gaps {sum(g for g in gaps if g > 0) / 1e3:.2f} ms (median gap {sorted(gaps)[len(gaps) // 2]:.2f} us)")
+fam = defaultdict(lambda: [0, 0.0])
+for a, b, nm in ks:
+    k = nm.replace("(anonymous namespace)::", "").replace("fde_b200::", "").replace("void ", "").split("(")[0][:50]
+    fam[k][0] += 1
+    fam[k][1] += b - a
+for k, (c, t) in sorted(fam.items(), key=lambda kv: -kv[1][1])[:25]:
+    print(f"  {t / 1e3 / steps:7.3f} ms/step {c // steps:5d} x {t / c:7.2f} us  {k}")

@@ -145,14 +145,38 @@ __device__ __forceinline__ void reduce_finish(double (&v)[NR], double* partials,
   }
 }
 
+// L2 eviction-priority hints for the Gram-Schmidt chain: w (read and written
+// every pass) and v_{k+1} (projected now, subtracted in the next pass) are
+// kept (evict_last); v_k has its last use of the pass (evict_first).  With
+// w and v_{k+1} L2-resident a pass streams one basis vector from HBM.
+__device__ __forceinline__ uint64_t policy_keep() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_stream() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 // out0 = ||w|| (sqrt of <w,w>), out1 = <v, w> in one pass over w (MGS start).
 __global__ void k_norm_dot(size_t n, const double* __restrict__ w, const double* __restrict__ v,
                            double* partials, unsigned int* counter, double* out0, double* out1) {
   double acc[2] = {0.0, 0.0};
+  const uint64_t keep = policy_keep();
   GRID_STRIDE(i, n) {
-    const double wi = w[i];
+    const double wi = ld_hint(w + i, keep);
     acc[0] = fma(wi, wi, acc[0]);
-    acc[1] = fma(v[i], wi, acc[1]);
+    acc[1] = fma(ld_hint(v + i, keep), wi, acc[1]);
   }
   double* const outs[2] = {out0, out1};
   const int sq[2] = {1, 0};
@@ -166,10 +190,12 @@ __global__ void k_mgs(size_t n, double* __restrict__ w, const double* __restrict
                       unsigned int* counter, double* out, int sqrt_out) {
   const double h = -*hk;
   double acc[1] = {0.0};
+  const bool last = vnext == w;
+  const uint64_t keep = policy_keep(), stream = policy_stream();
   GRID_STRIDE(i, n) {
-    const double wi = fma(h, vk[i], w[i]);  // kernels::axpy(-h, v_k, w) (AVX2 fma)
-    w[i] = wi;
-    acc[0] = fma(vnext == w ? wi : vnext[i], wi, acc[0]);
+    const double wi = fma(h, ld_hint(vk + i, stream), ld_hint(w + i, keep));  // axpy(-h, v_k, w)
+    st_hint(w + i, wi, keep);
+    acc[0] = fma(last ? wi : ld_hint(vnext + i, keep), wi, acc[0]);
   }
   double* const outs[1] = {out};
   const int sq[1] = {sqrt_out};

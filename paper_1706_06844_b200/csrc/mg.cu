@@ -203,7 +203,18 @@ void Hierarchy::vcycle(const double* b, double* x, bool zero_guess, cudaStream_t
   cycle(0, b, x, zero_guess, s);
 }
 
-void Hierarchy::cycle(size_t l, const double* b, double* x, bool zero, cudaStream_t s) const {
+// Does level l, entered with a zero guess, start with x = omega dinv b as a
+// separate pass (so the restriction producing b can write it instead)?
+bool Hierarchy::zero_guess_is_diag_scale(size_t l) const {
+  const LevelOp& lev = levels_[l];
+  const bool mapped = lev.sop && lev.sop->maps_input();
+  if (l + 1 == levels_.size())
+    return coarse_ == COARSE_SWEEPS && !(mapped && (fuse_ & 1) && coarse_sweeps_ > 1);
+  return !(mapped && (fuse_ & 1));
+}
+
+void Hierarchy::cycle(size_t l, const double* b, double* x, bool zero, cudaStream_t s,
+                      bool prescaled) const {
   const LevelOp& lev = levels_[l];
   const size_t n = lev.size();
   const double* dinv = dinv_[l].get();
@@ -243,7 +254,7 @@ void Hierarchy::cycle(size_t l, const double* b, double* x, bool zero, cudaStrea
       } else if (mapped && (fuse_ & 1) && coarse_sweeps_ > 1) {
         lev.sop->run_mapped(zin, x, x, 1.0, EPI_JACOBI, jac, s);  // first two sweeps
         k = 2;
-      } else {
+      } else if (!prescaled) {
         vec_diag_scale(n, omega_, dinv, b, x, s);
       }
       for (; k < coarse_sweeps_; ++k) sweep();
@@ -255,13 +266,22 @@ void Hierarchy::cycle(size_t l, const double* b, double* x, bool zero, cudaStrea
   if (zero && mapped && (fuse_ & 1)) {
     lev.sop->run_mapped(zin, x, r_[l].get(), 1.0, EPI_RESID, res, s);  // x, r = b - A x
   } else {
-    if (zero) vec_diag_scale(n, omega_, dinv, b, x, s);
-    else sweep();
+    if (zero) {
+      if (!prescaled) vec_diag_scale(n, omega_, dinv, b, x, s);
+    } else {
+      sweep();
+    }
     lev.run(x, r_[l].get(), EPI_RESID, res, s);  // r = b - A x
   }
-  xfer_restrict(xfer_[l], r_[l].get(), bc_[l + 1].get(), mode_ == MODE_GALERKIN ? 1.0 : 0.5, s);
+  const double rsc = mode_ == MODE_GALERKIN ? 1.0 : 0.5;
+  const bool fuse_smooth = zero_guess_is_diag_scale(l + 1);
+  if (fuse_smooth)
+    xfer_restrict_smooth(xfer_[l], r_[l].get(), bc_[l + 1].get(), rsc, dinv_[l + 1].get(), omega_,
+                         xc_[l + 1].get(), s);
+  else
+    xfer_restrict(xfer_[l], r_[l].get(), bc_[l + 1].get(), rsc, s);
   if (l + 2 == levels_.size() && coarse_ == COARSE_NONE) xc_[l + 1].zero(s);
-  cycle(l + 1, bc_[l + 1].get(), xc_[l + 1].get(), true, s);
+  cycle(l + 1, bc_[l + 1].get(), xc_[l + 1].get(), true, s, fuse_smooth);
   if (mapped && (fuse_ & 2)) {
     InMap pin{};
     pin.kind = 2;

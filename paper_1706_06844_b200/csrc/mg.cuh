@@ -66,7 +66,11 @@ class Hierarchy {
   void refactor_coarse(cudaStream_t s);
 
  private:
-  void cycle(size_t l, const double* b, double* x, bool zero, cudaStream_t s) const;
+  // prescaled: x already holds the zero-guess smoothing omega dinv b (fused
+  // into the restriction that produced b)
+  void cycle(size_t l, const double* b, double* x, bool zero, cudaStream_t s,
+             bool prescaled = false) const;
+  bool zero_guess_is_diag_scale(size_t l) const;
   std::vector<LevelOp> levels_;
   std::vector<std::pair<size_t, size_t>> dims_;
   std::vector<Xfer> xfer_;

@@ -214,8 +214,12 @@ __device__ __forceinline__ double rrow(const double* f, int n, int fc, double sc
 // Row windows let the same kernels run on a y-slab: the fine buffer holds
 // global fine rows [f_lo, f_lo + rows), the coarse buffer global coarse rows
 // [c_lo, c_lo + rows).  Full-grid calls use f_lo = c_lo = 0.
+// xs != nullptr: also x_c = (omega dinv_c) bc, the next level's zero-guess
+// smoothing (multigrid.cpp:355-356), in the same pass
 __global__ void k_restrict(Xfer t, const double* __restrict__ f, int f_lo,
-                           double* __restrict__ c, int c_lo, int c_rows, double sc) {
+                           double* __restrict__ c, int c_lo, int c_rows, double sc,
+                           double* __restrict__ xs = nullptr,
+                           const double* __restrict__ dinv = nullptr, double omega = 0.0) {
   const size_t nc = (size_t)t.k1 * c_rows;
   GRID_STRIDE(q, nc) {
     const int a = (int)(q % t.k1), bb = (int)(q / t.k1) + c_lo;  // global coarse row
@@ -237,6 +241,7 @@ __global__ void k_restrict(Xfer t, const double* __restrict__ f, int f_lo,
       out = v * sc;
     }
     c[q] = out;
+    if (xs) xs[q] = omega * dinv[q] * out;  // vec_diag_scale's (a d) b
   }
 }
 
@@ -388,6 +393,14 @@ void xfer_prolong_rows(const Xfer& t, const double* coarse, int c_lo, double* fi
 void xfer_restrict(const Xfer& t, const double* fine, double* coarse, double scale,
                    cudaStream_t s) {
   xfer_restrict_rows(t, fine, 0, coarse, 0, t.k2, scale, s);
+}
+void xfer_restrict_smooth(const Xfer& t, const double* fine, double* coarse, double scale,
+                          const double* dinv_c, double omega, double* xc, cudaStream_t s) {
+  const size_t nc = (size_t)t.k1 * t.k2;
+  if (!nc) return;
+  k_restrict<<<blocks_for(nc), kThreads, 0, s>>>(t, fine, 0, coarse, 0, t.k2, scale, xc, dinv_c,
+                                                 omega);
+  FDE_LAUNCH_CHECK();
 }
 void xfer_prolong_add(const Xfer& t, const double* coarse, double* fine, cudaStream_t s) {
   xfer_prolong_rows(t, coarse, 0, fine, 0, t.n2, true, s);

@@ -54,6 +54,9 @@ class Reducer {
 Xfer make_xfer(int n1, int n2, bool cx, bool cy);
 // coarse = scale-weighted transpose of prolongation (restrict_full: 0.5,
 // restrict_transpose: 1.0), same operation order as restrict_rows/cols.
+// restriction fused with the coarse level's zero-guess smoothing xc = omega dinv_c bc
+void xfer_restrict_smooth(const Xfer& t, const double* fine, double* coarse, double scale,
+                          const double* dinv_c, double omega, double* xc, cudaStream_t s);
 void xfer_restrict(const Xfer& t, const double* fine, double* coarse, double scale,
                    cudaStream_t s);
 // fine += P coarse (prolong then axpy 1.0, multigrid.cpp:377-378)

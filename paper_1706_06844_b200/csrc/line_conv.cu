@@ -666,7 +666,10 @@ struct LineIO<YPass, EPI> {
   }
   // the two operand streams staged through shared memory, and the rest
   __device__ __forceinline__ const double* staged(int k, int d) const { return (k ? em : ep) + d; }
-  __device__ __forceinline__ Ops fetch_rest(int, double s0, double s1) const { return Ops{s0, s1}; }
+  static constexpr bool kKeepX = false;  // the epilogue does not read x
+  __device__ __forceinline__ Ops fetch_rest(int, double s0, double s1, double) const {
+    return Ops{s0, s1};
+  }
   __device__ __forceinline__ Ops fetch(int d) const { return Ops{ep[d], em[d]}; }
   __device__ __forceinline__ void finish(int d, double ty, double tt, const Ops& o) const {
     const double v = c * (o.ep * ty + o.em * tt);
@@ -704,9 +707,11 @@ struct LineIO<XPass, EPI> {
   __device__ __forceinline__ double load(int d) const { return x[d]; }
   __device__ __forceinline__ const double* xaddr(int d) const { return x + d; }
   __device__ __forceinline__ const double* staged(int k, int d) const { return (k ? dm : dp) + d; }
-  __device__ __forceinline__ Ops fetch_rest(int d, double s0, double s1) const {
+  // the line's own input stays in shared memory for the epilogue (xv)
+  static constexpr bool kKeepX = true;
+  __device__ __forceinline__ Ops fetch_rest(int d, double s0, double s1, double xv) const {
     Ops o;
-    o.x = x[d];
+    o.x = xv;
     o.dp = s0;
     o.dm = s1;
     o.q = q ? q[d] : 0.0;
@@ -799,7 +804,7 @@ __global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THRE
       v[s] = t;
       v[s + H] = make_double2(0.0, 0.0);
     }
-    if (line + (int)gridDim.x < nl) prefetch_x(line + gridDim.x);
+    if (!IO::kKeepX && line + (int)gridDim.x < nl) prefetch_x(line + gridDim.x);
 
     // 2) forward transform; ends with this thread's paired slots in v
     double2 w1s[P];
@@ -900,12 +905,14 @@ __global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THRE
           const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
           const double2 a = *reinterpret_cast<const double2*>(ep0 + i0);
           const double2 b = *reinterpret_cast<const double2*>(ep1 + i0);
+          const double2 xv = IO::kKeepX ? *reinterpret_cast<const double2*>(xbuf + i0)
+                                        : make_double2(0.0, 0.0);
 #ifdef FDE_EXP_NOEPI
           o[2 * c] = typename IO::Ops{a.x, b.x};
           o[2 * c + 1] = typename IO::Ops{a.y, b.y};
 #else
-          o[2 * c] = io.fetch_rest(d, a.x, b.x);
-          o[2 * c + 1] = io.fetch_rest(d + 1, a.y, b.y);
+          o[2 * c] = io.fetch_rest(d, a.x, b.x, xv.x);
+          o[2 * c + 1] = io.fetch_rest(d + 1, a.y, b.y, xv.y);
 #endif
         }
 #pragma unroll
@@ -919,12 +926,15 @@ __global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THRE
         for (int c = 0; c < 4; ++c) {
           const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
           if (i0 < n)
-            io.finish(d, ty[c].x, v[g + c].x, io.fetch_rest(d, ep0[i0], ep1[i0]));
+            io.finish(d, ty[c].x, v[g + c].x, io.fetch_rest(d, ep0[i0], ep1[i0], xbuf[i0]));
           if (i0 + 1 < n)
-            io.finish(d + 1, ty[c].y, v[g + c].y, io.fetch_rest(d + 1, ep0[i0 + 1], ep1[i0 + 1]));
+            io.finish(d + 1, ty[c].y, v[g + c].y,
+                      io.fetch_rest(d + 1, ep0[i0 + 1], ep1[i0 + 1], xbuf[i0 + 1]));
         }
       }
     }
+    // row pass: the next line's input lands once this line's epilogue is done
+    if (IO::kKeepX && line + (int)gridDim.x < nl) prefetch_x(line + gridDim.x);
   }
   tmem_fence_before();
   __syncthreads();

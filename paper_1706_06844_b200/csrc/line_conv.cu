@@ -144,6 +144,65 @@ struct Dft<16, INV, HALF> {
   }
 };
 
+// Output-pruned DFTs: only outputs 0 .. R/2 - 1 (the last inverse stage, whose
+// upper half lands on positions >= M/2 that the zero-padded lines discard).
+template <bool INV>
+__device__ __forceinline__ void dft4_lo(double2& a0, double2& a1, double2 a2, double2 a3) {
+  const double2 b0 = cadd(a0, a2), b2 = csub(a0, a2);
+  const double2 b1 = cadd(a1, a3), b3 = rot90<INV>(csub(a1, a3));
+  a0 = cadd(b0, b1);
+  a1 = cadd(b2, b3);
+}
+template <int R, bool INV>
+struct DftLo;
+template <bool INV>
+struct DftLo<8, INV> {
+  __device__ __forceinline__ static void run(double2 (&u)[8]) {
+    double2 a[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      a[k] = cadd(u[k], u[k + 4]);
+      a[k + 4] = csub(u[k], u[k + 4]);
+    }
+    a[5] = tw16<INV, 2>(a[5]);
+    a[6] = tw16<INV, 4>(a[6]);
+    a[7] = tw16<INV, 6>(a[7]);
+    dft4_lo<INV>(a[0], a[1], a[2], a[3]);  // X[0], X[2]
+    dft4_lo<INV>(a[4], a[5], a[6], a[7]);  // X[1], X[3]
+    u[0] = a[0]; u[2] = a[1];
+    u[1] = a[4]; u[3] = a[5];
+  }
+};
+template <bool INV>
+struct DftLo<16, INV> {
+  __device__ __forceinline__ static void run(double2 (&u)[16]) {
+    double2 a[4][4];  // a[n1][k1]
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) {
+      a[n1][0] = u[n1];
+      a[n1][1] = u[n1 + 4];
+      a[n1][2] = u[n1 + 8];
+      a[n1][3] = u[n1 + 12];
+      dft4<INV>(a[n1][0], a[n1][1], a[n1][2], a[n1][3]);
+    }
+    a[1][1] = tw16<INV, 1>(a[1][1]);
+    a[1][2] = tw16<INV, 2>(a[1][2]);
+    a[1][3] = tw16<INV, 3>(a[1][3]);
+    a[2][1] = tw16<INV, 2>(a[2][1]);
+    a[2][2] = tw16<INV, 4>(a[2][2]);
+    a[2][3] = tw16<INV, 6>(a[2][3]);
+    a[3][1] = tw16<INV, 3>(a[3][1]);
+    a[3][2] = tw16<INV, 6>(a[3][2]);
+    a[3][3] = tw16<INV, 9>(a[3][3]);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      dft4_lo<INV>(a[0][k1], a[1][k1], a[2][k1], a[3][k1]);
+      u[k1] = a[0][k1];
+      u[k1 + 4] = a[1][k1];
+    }
+  }
+};
+
 template <int R>
 struct Log2;
 template <> struct Log2<2> { static constexpr int v = 1; };
@@ -457,7 +516,7 @@ __device__ __forceinline__ int paired_bfly(int tl, int q) {
 }
 
 // twiddle + DFT of this thread's B = P / R butterflies (slots q + r * B)
-template <int LOGM, int P, bool INV, int NSL, int R, bool PAIRED, bool HALF>
+template <int LOGM, int P, bool INV, int NSL, int R, bool PAIRED, bool HALF, bool LOWOUT = false>
 __device__ __forceinline__ void pstage_compute(double2 (&v)[P], int tl, const double2 (&w1s)[P]) {
 #ifdef FDE_EXP_NOFFT
   return;
@@ -476,9 +535,15 @@ __device__ __forceinline__ void pstage_compute(double2 (&v)[P], int tl, const do
 #pragma unroll
       for (int r = 1; r < R; ++r) u[r] = cmul(u[r], w[r]);
     }
-    Dft<R, INV, HALF>::run(u);
+    if constexpr (LOWOUT) {
+      DftLo<R, INV>::run(u);
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[q + r * B] = u[r];
+      for (int r = 0; r < R / 2; ++r) v[q + r * B] = u[r];
+    } else {
+      Dft<R, INV, HALF>::run(u);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[q + r * B] = u[r];
+    }
   }
 }
 
@@ -544,6 +609,9 @@ __device__ __forceinline__ void pstage_read(double2 (&v)[P], const double* re, c
   }
 }
 
+#ifndef FDE_PRUNE_LAST
+#define FDE_PRUNE_LAST 1
+#endif
 // Forward transform, radix-P stages from NSL, ending with the paired R0 stage.
 // On entry the stage at NSL has its inputs in v; the exchange buffer toggles.
 template <int LOGM, int P, int NSL, bool HALF>
@@ -587,7 +655,9 @@ struct PInvTail {
                                              const Hook& hook) {
     using S = PairedShape<LOGM, P>;
     constexpr int LP = S::LP;
-    pstage_compute<LOGM, P, true, NSL, P, false, false>(v, tl, w1s);
+    // last stage: slots q + r B with r >= P/2 hold positions >= M/2 (unused)
+    pstage_compute<LOGM, P, true, NSL, P, false, false, (NSL + LP >= LOGM) && FDE_PRUNE_LAST>(
+        v, tl, w1s);
     if constexpr (NSL + LP < LOGM) {
       double* re = buf + cur * 2 * S::BUF;
       if constexpr (S::NBUF == 1) __syncthreads();
@@ -752,7 +822,10 @@ __global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THRE
   constexpr int T = S::T, H = P / 2, R0 = S::R0, B0 = S::B0, NS0 = S::NS0;
   extern __shared__ __align__(16) double smem[];
   double* const xbuf = smem + S::NBUF * 2 * S::BUF;  // next line's input (own slots only)
-  __shared__ uint32_t s_tbase;
+  // the TMEM base address lands in the first exchange-buffer word (read into a
+  // register before any exchange): no static shared memory, so four CTAs fit
+  // a 196 KB carveout and the rest of the SM's L1 caches the spectral tables
+  uint32_t* const s_tbase = reinterpret_cast<uint32_t*>(smem);
   const int tl = threadIdx.x, warp = tl >> 5;
   const int n = p.blk.n, nl = p.nlines();
 
@@ -778,12 +851,14 @@ __global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THRE
     for (int k = 0; k < slot; ++k) __nanosleep(FDE_EXP_STAGGER);
   }
 #endif
-  if (warp == 0) tmem_alloc<S::TCOLS>(&s_tbase);
+  if (warp == 0) tmem_alloc<S::TCOLS>(s_tbase);
   if (blockIdx.x < nl) prefetch_x(blockIdx.x);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  const uint32_t tq = s_tbase + ((uint32_t)(warp * 32) << 16);  // this warp's lane quadrant
+  const uint32_t tbase = *s_tbase;  // the first exchange write follows a barrier
+  if constexpr (S::NBUF != 1) __syncthreads();
+  const uint32_t tq = tbase + ((uint32_t)(warp * 32) << 16);  // this warp's lane quadrant
   const uint32_t tqy = tq, tqt = tq + 4 * P;                    // Qy, Qt column ranges
   const double* const ep0 = smem;            // staged epilogue operands (exchange buffer)
   const double* const ep1 = smem + S::BUF;
@@ -892,45 +967,38 @@ __global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THRE
       }
     }
 
-    // 6) epilogue in groups of 4 slots (8 positions); own staged slots only
+    // 6) epilogue in groups of 4 slots (8 positions); own staged slots only.
+    //    Every operand of a group is fetched before any of its stores, with
+    //    out-of-range positions clamped to the thread's first position
+    //    (2 tl < n) and only the stores predicated: the global loads of a
+    //    group are all in flight together (a tail group fetched element by
+    //    element behind its own stores serialised one L2 latency per load).
     cp_async_wait_all();
 #pragma unroll
     for (int g = 0; g < H; g += 4) {
       double2 ty[4];
       tmem_ld4(tqy + 4 * g, ty);
       typename IO::Ops o[8];
-      if (2 * T * (g + 4) <= n) {  // whole group in range for every thread (uniform)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
-          const double2 a = *reinterpret_cast<const double2*>(ep0 + i0);
-          const double2 b = *reinterpret_cast<const double2*>(ep1 + i0);
-          const double2 xv = IO::kKeepX ? *reinterpret_cast<const double2*>(xbuf + i0)
-                                        : make_double2(0.0, 0.0);
+      for (int c = 0; c < 4; ++c) {
+        const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
+        const double2 a = *reinterpret_cast<const double2*>(ep0 + i0);
+        const double2 b = *reinterpret_cast<const double2*>(ep1 + i0);
+        const double2 xv = IO::kKeepX ? *reinterpret_cast<const double2*>(xbuf + i0)
+                                      : make_double2(0.0, 0.0);
 #ifdef FDE_EXP_NOEPI
-          o[2 * c] = typename IO::Ops{a.x, b.x};
-          o[2 * c + 1] = typename IO::Ops{a.y, b.y};
+        o[2 * c] = typename IO::Ops{a.x, b.x};
+        o[2 * c + 1] = typename IO::Ops{a.y, b.y};
 #else
-          o[2 * c] = io.fetch_rest(d, a.x, b.x, xv.x);
-          o[2 * c + 1] = io.fetch_rest(d + 1, a.y, b.y, xv.y);
+        o[2 * c] = io.fetch_rest(i0 < n ? d : 0, a.x, b.x, xv.x);
+        o[2 * c + 1] = io.fetch_rest(i0 + 1 < n ? d + 1 : 0, a.y, b.y, xv.y);
 #endif
-        }
+      }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int d = 2 * (g + c) * T;
-          io.finish(d, ty[c].x, v[g + c].x, o[2 * c]);
-          io.finish(d + 1, ty[c].y, v[g + c].y, o[2 * c + 1]);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
-          if (i0 < n)
-            io.finish(d, ty[c].x, v[g + c].x, io.fetch_rest(d, ep0[i0], ep1[i0], xbuf[i0]));
-          if (i0 + 1 < n)
-            io.finish(d + 1, ty[c].y, v[g + c].y,
-                      io.fetch_rest(d + 1, ep0[i0 + 1], ep1[i0 + 1], xbuf[i0 + 1]));
-        }
+      for (int c = 0; c < 4; ++c) {
+        const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
+        if (i0 < n) io.finish(d, ty[c].x, v[g + c].x, o[2 * c]);
+        if (i0 + 1 < n) io.finish(d + 1, ty[c].y, v[g + c].y, o[2 * c + 1]);
       }
     }
     // row pass: the next line's input lands once this line's epilogue is done
@@ -938,7 +1006,7 @@ __global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THRE
   }
   tmem_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<S::TCOLS>(s_tbase);
+  if (warp == 0) tmem_dealloc<S::TCOLS>(tbase);
 }
 
 // Warp-per-line direct Toeplitz product for short lines (n <= kDirectMax):
@@ -1071,6 +1139,13 @@ void launch_fft(const P& p, cudaStream_t s) {
 #define FDE_PAIRED 1
 #endif
 
+// Shared-memory carveout (percent of the 228 KB maximum): 85 % selects the
+// 196 KB configuration, which still holds four CTAs (4 x 49,152 B + 1 KB
+// reserved each) and leaves 60 KB of L1 for the spectral constants and
+// twiddles (measured 165 -> 160 us per n = 2047 apply against the maximum).
+#ifndef FDE_PAIRED_CARVEOUT
+#define FDE_PAIRED_CARVEOUT 85
+#endif
 template <int LOGM, class P, int EPI>
 void launch_paired_epi(const P& p, cudaStream_t s) {
   constexpr int PP = LOGM >= 11 ? 16 : 8;
@@ -1082,7 +1157,7 @@ void launch_paired_epi(const P& p, cudaStream_t s) {
     // resident CTAs are register-bound; give shared memory the whole carveout
     FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
                                   cudaFuncAttributePreferredSharedMemoryCarveout,
-                                  (int)cudaSharedmemCarveoutMaxShared));
+                                  FDE_PAIRED_CARVEOUT));
     configured = true;
   }
   static int max_ctas = 0;  // resident CTAs on the device (persistent grid)

@@ -35,3 +35,22 @@ for a, b, nm in ks:
     fam[k][1] += b - a
 for k, (c, t) in sorted(fam.items(), key=lambda kv: -kv[1][1])[:25]:
     print(f"  {t / 1e3 / steps:7.3f} ms/step {c // steps:5d} x {t / c:7.2f} us  {k}")
+# coarse-tail segments: maximal runs of short kernels (< 12 us), span incl. gaps
+runs, cur = [], None
+for a, b, nm in ks:
+    if b - a < 12.0:
+        cur = [a, b, 1] if cur is None else [cur[0], b, cur[2] + 1]
+    else:
+        if cur is not None and cur[2] >= 3:
+            runs.append(cur)
+        cur = None
+if cur is not None and cur[2] >= 3:
+    runs.append(cur)
+tail = sum(b - a for a, b, _ in runs)
+print(f"short-kernel runs (>=3 consecutive kernels < 12 us): {len(runs) // steps}/step, "
+      f"{tail / 1e3 / steps:.3f} ms/step span, {sum(c for *_, c in runs) // steps} kernels/step")
+big = [g for g in gaps if g > 5.0]
+print(f"gaps > 5 us: {len(big) // steps}/step, {sum(big) / 1e3 / steps:.3f} ms/step; "
+      f"gaps <= 5 us: {sum(g for g in gaps if 0 < g <= 5.0) / 1e3 / steps:.3f} ms/step")
+small = [b - a for a, b, _ in ks if b - a < 12.0]
+print(f"kernels < 12 us: {len(small) // steps}/step, {sum(small) / 1e3 / steps:.3f} ms/step busy")

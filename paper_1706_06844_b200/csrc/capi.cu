@@ -12,6 +12,13 @@
 
 namespace fde_b200 {
 std::atomic<unsigned long long> g_kernel_launches{0};
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FDE_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 }
 
 using namespace fde_b200;

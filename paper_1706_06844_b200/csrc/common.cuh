@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 namespace fde_b200 {
 
@@ -34,6 +35,38 @@ extern std::atomic<unsigned long long> g_kernel_launches;
     ::fde_b200::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \
     ::fde_b200::cuda_check(cudaGetLastError(), "kernel launch");            \
   } while (0)
+
+// ---- programmatic dependent launch ---------------------------------------
+// Every kernel is launched with programmatic stream serialization and opens
+// with pdl_enter(): it lets the next kernel in the stream (or captured graph)
+// be launched as soon as all of this grid's CTAs are running, then waits for
+// the previous kernel to complete and flush before touching memory.  Kernel
+// boundaries then overlap launch processing and CTA dispatch with the tail of
+// the previous grid (the V-cycle's coarse levels are chains of short kernels).
+// FDE_PDL=0 in the environment launches plainly (the waits become no-ops).
+__device__ __forceinline__ void pdl_enter() {
+#if defined(__CUDA_ARCH__)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t s, Args&&... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cuda_check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "kernel launch");
+}
 
 // ---- complex helpers on double2 (x = re, y = im) ---------------------------
 __host__ __device__ __forceinline__ double2 cadd(double2 a, double2 b) {

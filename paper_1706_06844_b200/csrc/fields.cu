@@ -22,6 +22,7 @@ __global__ void k_example_fields(ExampleSpec e, int n1, int n2, double gx0, doub
                                  double gy0, double hy, double t, double* __restrict__ dp,
                                  double* __restrict__ dm, double* __restrict__ ep,
                                  double* __restrict__ em) {
+  pdl_enter();
   const size_t n = (size_t)n1 * n2;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n;
        q += (size_t)gridDim.x * blockDim.x) {
@@ -36,6 +37,7 @@ __global__ void k_example_fields(ExampleSpec e, int n1, int n2, double gx0, doub
 
 __global__ void k_example_source(ExampleSpec e, int n1, int n2, double gx0, double hx,
                                  double gy0, double hy, double t, double* __restrict__ v) {
+  pdl_enter();
   const size_t n = (size_t)n1 * n2;
   for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n;
        q += (size_t)gridDim.x * blockDim.x) {
@@ -52,6 +54,7 @@ constexpr int kSumBlocks = 296;
 __global__ void k_pair_sums(size_t n, const double* __restrict__ a, const double* __restrict__ b,
                             const double* __restrict__ c, const double* __restrict__ d,
                             double* __restrict__ part) {
+  pdl_enter();
   __shared__ double s1[kThreads], s2[kThreads];
   const size_t chunk = (n + gridDim.x - 1) / gridDim.x;
   const size_t lo = blockIdx.x * chunk, hi = lo + chunk < n ? lo + chunk : n;
@@ -99,7 +102,7 @@ void FieldScratch::ensure(size_t n) {
 
 double anisotropy_ratio_device(FieldScratch& f, size_t n, double s_over_r, double alpha,
                                double beta, cudaStream_t s) {
-  k_pair_sums<<<kSumBlocks, kThreads, 0, s>>>(n, f.dp.get(), f.dm.get(), f.ep.get(), f.em.get(),
+  launch_k(k_pair_sums, kSumBlocks, kThreads, 0, s, n, f.dp.get(), f.dm.get(), f.ep.get(), f.em.get(),
                                               f.partial.get());
   FDE_LAUNCH_CHECK();
   std::vector<double> part(2 * kSumBlocks);
@@ -157,7 +160,7 @@ void sample_fields_device(const Problem& p, const Grid& g, size_t m, double* dp,
   const double t = static_cast<double>(m) * g.dt;  // problem.cpp:52
   const size_t n = g.size();
   if (p.example.which) {
-    k_example_fields<<<blocks_for(n), kThreads, 0, s>>>(p.example, (int)g.n1, (int)g.n2, g.ax,
+    launch_k(k_example_fields, blocks_for(n), kThreads, 0, s, p.example, (int)g.n1, (int)g.n2, g.ax,
                                                         g.hx, g.ay, g.hy, t, dp, dm, ep, em);
     FDE_LAUNCH_CHECK();
     return;
@@ -187,7 +190,7 @@ void example_source_device(const Problem& p, const Grid& g, size_t m, double* v,
                            cudaStream_t s) {
   if (!p.example.which) throw InvalidArgument("not an example problem");
   const double t_half = (static_cast<double>(m) - 0.5) * g.dt;  // problem.cpp:81
-  k_example_source<<<blocks_for(g.size()), kThreads, 0, s>>>(
+  launch_k(k_example_source, blocks_for(g.size()), kThreads, 0, s, 
       p.example, (int)g.n1, (int)g.n2, g.ax, g.hx, g.ay, g.hy, t_half, v);
   FDE_LAUNCH_CHECK();
 }

@@ -10,6 +10,7 @@ namespace {
 
 __global__ void k_copy_scale(size_t n, double a, const double* __restrict__ x,
                              double* __restrict__ y) {
+  pdl_enter();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
     y[i] = x[i] * a;
@@ -17,13 +18,14 @@ __global__ void k_copy_scale(size_t n, double a, const double* __restrict__ x,
 void copy_scale(size_t n, double a, const double* x, double* y, cudaStream_t s) {
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_copy_scale<<<blocks, 256, 0, s>>>(n, a, x, y);
+  launch_k(k_copy_scale, blocks, 256, 0, s, n, a, x, y);
   FDE_LAUNCH_CHECK();
 }
 
 // p = r + beta (p - omega v)     (BiCGSTAB direction update)
 __global__ void k_bicg_p(size_t n, double beta, double omg, const double* __restrict__ r,
                          const double* __restrict__ v, double* __restrict__ p) {
+  pdl_enter();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
     p[i] = r[i] + beta * (p[i] - omg * v[i]);
@@ -31,6 +33,7 @@ __global__ void k_bicg_p(size_t n, double beta, double omg, const double* __rest
 // s = r - alpha v
 __global__ void k_axpy2(size_t n, double a, const double* __restrict__ x,
                         const double* __restrict__ y, double* __restrict__ out) {
+  pdl_enter();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
     out[i] = y[i] - a * x[i];
@@ -38,6 +41,7 @@ __global__ void k_axpy2(size_t n, double a, const double* __restrict__ x,
 // x += alpha p + omega s
 __global__ void k_bicg_x(size_t n, double alpha, double omg, const double* __restrict__ p,
                          const double* __restrict__ sv, double* __restrict__ x) {
+  pdl_enter();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
     x[i] += alpha * p[i] + omg * sv[i];
@@ -47,16 +51,18 @@ __global__ void k_bicg_x(size_t n, double alpha, double omg, const double* __res
 // per-iteration round trip never queues behind bulk host copies running on
 // other streams (the march's pipelined source / solution transfers).
 __global__ void k_copy_small(double* __restrict__ dst, const double* __restrict__ src, int n) {
+  pdl_enter();
   for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 void copy_small(double* dst, const double* src, size_t n, cudaStream_t s) {
-  k_copy_small<<<1, 128, 0, s>>>(dst, src, (int)n);
+  launch_k(k_copy_small, 1, 128, 0, s, dst, src, (int)n);
   FDE_LAUNCH_CHECK();
 }
 
 // device-to-device vector copy on the SMs (a DMA copy would queue behind the
 // march's bulk host transfers on the copy engines)
 __global__ void k_copy(size_t n, const double* __restrict__ x, double* __restrict__ y) {
+  pdl_enter();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
     y[i] = x[i];
@@ -64,7 +70,7 @@ __global__ void k_copy(size_t n, const double* __restrict__ x, double* __restric
 void copy_vec(size_t n, const double* x, double* y, cudaStream_t s) {
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_copy<<<blocks ? blocks : 1, 256, 0, s>>>(n, x, y);
+  launch_k(k_copy, blocks ? blocks : 1, 256, 0, s, n, x, y);
   FDE_LAUNCH_CHECK();
 }
 
@@ -370,7 +376,7 @@ KrylovResult KrylovWorkspace::bicgstab(const StructuredOp& a, const Precond* m,
       copy_vec(n, r, p, s);
     } else {
       const double beta = (rho_new / rho) * (alpha / omg);
-      k_bicg_p<<<nblocks(n), 256, 0, s>>>(n, beta, omg, r, v, p);
+      launch_k(k_bicg_p, nblocks(n), 256, 0, s, n, beta, omg, r, v, p);
       FDE_LAUNCH_CHECK();
     }
     a.apply(p, tmp, s);
@@ -378,7 +384,7 @@ KrylovResult KrylovWorkspace::bicgstab(const StructuredOp& a, const Precond* m,
     const double rv = dot_host(rh, v, s);
     if (rv == 0.0) break;
     alpha = rho_new / rv;
-    k_axpy2<<<nblocks(n), 256, 0, s>>>(n, alpha, v, r, sv);  // s = r - alpha v
+    launch_k(k_axpy2, nblocks(n), 256, 0, s, n, alpha, v, r, sv);  // s = r - alpha v
     FDE_LAUNCH_CHECK();
     ++res.total_iterations;
     const double srel = nrm2_host(sv, s) / norm_b;
@@ -398,9 +404,9 @@ KrylovResult KrylovWorkspace::bicgstab(const StructuredOp& a, const Precond* m,
     precondition(m, tmp, tv, s);
     const double tt = dot_host(tv, tv, s);
     omg = tt > 0.0 ? dot_host(tv, sv, s) / tt : 0.0;
-    k_bicg_x<<<nblocks(n), 256, 0, s>>>(n, alpha, omg, p, sv, x);
+    launch_k(k_bicg_x, nblocks(n), 256, 0, s, n, alpha, omg, p, sv, x);
     FDE_LAUNCH_CHECK();
-    k_axpy2<<<nblocks(n), 256, 0, s>>>(n, omg, tv, sv, r);  // r = s - omega t
+    launch_k(k_axpy2, nblocks(n), 256, 0, s, n, omg, tv, sv, r);  // r = s - omega t
     FDE_LAUNCH_CHECK();
     rho = rho_new;
     const double rel = nrm2_host(r, s) / norm_b;

@@ -357,6 +357,7 @@ struct FftShape {
 template <int LOGM, class Pol>
 __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
     fft_line_kernel(const Pol p) {
+  pdl_enter();
   using S = FftShape<LOGM>;
   constexpr int M = S::M, T = S::T, BUF = S::BUF, P = S::P, H = P / 2, SH = Log2<P>::v;
   extern __shared__ double smem[];
@@ -816,6 +817,7 @@ template <int LOGM, class Pol, int EPI>
 __global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THREADS,
                                   LOGM >= 11 ? FDE_PAIRED_MINB : FDE_PAIRED_MINB10)
     fft_line_kernel_paired(const Pol p) {
+  pdl_enter();
   constexpr int P = LOGM >= 11 ? 16 : 8;
   using S = PairedShape<LOGM, P>;
   using IO = LineIO<Pol, EPI>;
@@ -1015,6 +1017,7 @@ __global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THRE
 // this is what the coarse multigrid levels run.
 template <class P>
 __global__ void __launch_bounds__(256) direct_line_kernel(const P p) {
+  pdl_enter();
   constexpr int E = kDirectMax / 32;
   __shared__ double s_col[kDirectMax], s_row[kDirectMax];
   const int n = p.blk.n;
@@ -1061,6 +1064,7 @@ __global__ void __launch_bounds__(256) direct_line_kernel(const P p) {
 // 32 x 32 tiles, 32 x 8 threads; padded shared tile (8-byte banks).
 __global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict__ in,
                                                         double* __restrict__ out, int n1, int n2) {
+  pdl_enter();
   __shared__ double tile[32][33];
   const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -1083,6 +1087,7 @@ template <int K>
 __global__ void __launch_bounds__(256) transpose_map_kernel(const InMap m, double* xout,
                                                             double* __restrict__ out, int n1,
                                                             int n2) {
+  pdl_enter();
   __shared__ double tile[32][33];
   const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -1131,7 +1136,7 @@ void launch_fft(const P& p, cudaStream_t s) {
   while (lpb > min_lpb && (lines + lpb - 1) / lpb < 2 * sms) lpb /= 2;
   const int grid = (lines + lpb - 1) / lpb;
   const size_t smem = size_t(lpb) * 2 * S::BUF * sizeof(double);
-  fft_line_kernel<LOGM, P><<<grid, S::T * lpb, smem, s>>>(p);
+  launch_k(fft_line_kernel<LOGM, P>, grid, S::T * lpb, smem, s, p);
   FDE_LAUNCH_CHECK();
 }
 
@@ -1181,8 +1186,8 @@ void launch_paired_epi(const P& p, cudaStream_t s) {
     max_ctas = sms * (per_sm > 0 ? per_sm : 1);
   }
   const int lines = lines_of(p);
-  fft_line_kernel_paired<LOGM, P, EPI><<<lines < max_ctas ? lines : max_ctas, S::THREADS,
-                                         S::SMEM, s>>>(p);
+  launch_k(fft_line_kernel_paired<LOGM, P, EPI>, lines < max_ctas ? lines : max_ctas, S::THREADS,
+                                         S::SMEM, s, p);
   FDE_LAUNCH_CHECK();
 }
 
@@ -1211,7 +1216,7 @@ void launch_any(const P& p, cudaStream_t s) {
   if (lines <= 0) return;
   switch (p.blk.logM) {
     case 0:
-      direct_line_kernel<P><<<(lines + 7) / 8, 256, 0, s>>>(p);
+      launch_k(direct_line_kernel<P>, (lines + 7) / 8, 256, 0, s, p);
       FDE_LAUNCH_CHECK();
       return;
     case 6: return launch_fft<6>(p, s);
@@ -1230,16 +1235,16 @@ void launch_any(const P& p, cudaStream_t s) {
 void launch_line_pass(const YPass& p, cudaStream_t s) { launch_any(p, s); }
 void launch_transpose(const double* in, double* out, int n1, int n2, cudaStream_t s) {
   const dim3 grid((n1 + 31) / 32, (n2 + 31) / 32);
-  transpose_kernel<<<grid, 256, 0, s>>>(in, out, n1, n2);
+  launch_k(transpose_kernel, grid, 256, 0, s, in, out, n1, n2);
   FDE_LAUNCH_CHECK();
 }
 void launch_transpose_mapped(const InMap& m, double* xout, double* out, int n1, int n2,
                              cudaStream_t s) {
   const dim3 grid((n1 + 31) / 32, (n2 + 31) / 32);
   switch (m.kind) {
-    case 0: transpose_map_kernel<0><<<grid, 256, 0, s>>>(m, xout, out, n1, n2); break;
-    case 1: transpose_map_kernel<1><<<grid, 256, 0, s>>>(m, xout, out, n1, n2); break;
-    case 2: transpose_map_kernel<2><<<grid, 256, 0, s>>>(m, xout, out, n1, n2); break;
+    case 0: launch_k(transpose_map_kernel<0>, grid, 256, 0, s, m, xout, out, n1, n2); break;
+    case 1: launch_k(transpose_map_kernel<1>, grid, 256, 0, s, m, xout, out, n1, n2); break;
+    case 2: launch_k(transpose_map_kernel<2>, grid, 256, 0, s, m, xout, out, n1, n2); break;
     default: throw InvalidArgument("unknown operator input map");
   }
   FDE_LAUNCH_CHECK();

@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstdlib>
@@ -128,6 +129,7 @@ void lu_factor(std::vector<double>& a, size_t n, std::vector<int>& perm) {
 
 __global__ void k_jacobi_update(size_t n, double omega, const double* __restrict__ dinv,
                                 const double* __restrict__ r, double* __restrict__ x) {
+  pdl_enter();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
     x[i] += omega * dinv[i] * r[i];
@@ -185,6 +187,79 @@ Hierarchy::Hierarchy(std::vector<LevelOp> levels, std::vector<std::pair<size_t, 
     lu_.upload(a.data(), a.size());
     perm_.upload(perm.data(), perm.size());
   }
+  plan_tail();
+}
+
+// The tail starts at the first level from which every level is structured,
+// small (kTailMaxN unknowns, kTailMaxLine per line) and fits the shared-memory
+// budget with its iterate, right-hand side and diagonal tables, and the
+// coarsest solve is sweeps or none.  Level 0 joins only for zero-guess cycles.
+void Hierarchy::plan_tail() {
+  tail_ = 0;
+  if (const char* e = std::getenv("FDE_MG_TAIL"))
+    if (e[0] == '0') return;
+  if (coarse_ == COARSE_LU) return;
+  size_t max_n = kTailMaxN;
+  if (const char* e = std::getenv("FDE_MG_TAIL_N")) max_n = std::min<size_t>(std::atol(e), max_n);
+  const size_t L = levels_.size();
+  size_t start = L, need = 0;
+  while (start > 0) {
+    const size_t l = start - 1;
+    const auto [n1, n2] = dims_[l];
+    const size_t n = n1 * n2;
+    // this level's x, b and tables; two scratch vectors of the first level's size
+    const size_t with = need + 2 * n + (2 * n1 - 1) + (2 * n2 - 1);
+    if (!levels_[l].sop || n > max_n || n1 > (size_t)kTailMaxLine ||
+        n2 > (size_t)kTailMaxLine || L - l > (size_t)kTailMaxLevels ||
+        with + 2 * n > (size_t)kTailSmemMax)
+      break;
+    need = with;
+    start = l;
+  }
+  if (start >= L) return;
+  if (start + 1 == L && coarse_ == COARSE_NONE) return;  // nothing to run
+  TailDesc& d = tail_desc_;
+  d = TailDesc{};
+  d.nl = (int)(L - start);
+  d.coarse = coarse_;
+  d.sweeps = (int)coarse_sweeps_;
+  d.omega = omega_;
+  d.rsc = mode_ == MODE_GALERKIN ? 1.0 : 0.5;
+  int off = 0;
+  auto take = [&](size_t n) {
+    const int o = off;
+    off += (int)((n + 1) & ~size_t(1));  // 16-byte aligned vectors
+    return o;
+  };
+  const size_t n0 = dims_[start].first * dims_[start].second;
+  d.s0 = take(n0);
+  d.s1 = take(n0);
+  for (size_t l = start; l < L; ++l) {
+    const StructuredOp& o = *levels_[l].sop;
+    TailLevel& t = d.lv[l - start];
+    t.n1 = (int)dims_[l].first;
+    t.n2 = (int)dims_[l].second;
+    t.inv_r = o.inv_r();
+    t.sr = o.s_over_r();
+    const LineBlockDev bx = o.block_x().dev(), by = o.block_y().dev();
+    t.colx = bx.col;
+    t.rowx = bx.row;
+    t.coly = by.col;
+    t.rowy = by.row;
+    t.dp = o.dp_dev();
+    t.dm = o.dm_dev();
+    t.epT = o.epT_dev();
+    t.emT = o.emT_dev();
+    t.dinv = dinv_[l].get();
+    t.xo = take((size_t)t.n1 * t.n2);
+    t.bo = take((size_t)t.n1 * t.n2);
+    t.tabx = take(2 * (size_t)t.n1 - 1);
+    t.taby = take(2 * (size_t)t.n2 - 1);
+    if (l + 1 < L) t.t = xfer_[l];
+  }
+  d.smem = off;
+  if (off > kTailSmemMax) return;
+  tail_ = start == 0 ? L : start;  // L marks "level 0" (0 means no tail)
 }
 
 void Hierarchy::refactor_coarse(cudaStream_t s) {
@@ -215,6 +290,14 @@ bool Hierarchy::zero_guess_is_diag_scale(size_t l) const {
 
 void Hierarchy::cycle(size_t l, const double* b, double* x, bool zero, cudaStream_t s,
                       bool prescaled) const {
+  if (tail_ && zero && l == (tail_ == levels_.size() ? 0 : tail_)) {
+    TailDesc d = tail_desc_;
+    d.b = b;
+    d.x = x;
+    d.prescaled = prescaled ? 1 : 0;
+    launch_vcycle_tail(d, s);
+    return;
+  }
   const LevelOp& lev = levels_[l];
   const size_t n = lev.size();
   const double* dinv = dinv_[l].get();
@@ -230,7 +313,7 @@ void Hierarchy::cycle(size_t l, const double* b, double* x, bool zero, cudaStrea
       lev.run(x, r_[l].get(), EPI_RESID, jac, s);
       int blocks = (int)((n + 255) / 256);
       if (blocks > 148 * 8) blocks = 148 * 8;
-      k_jacobi_update<<<blocks, 256, 0, s>>>(n, omega_, dinv, r_[l].get(), x);
+      launch_k(k_jacobi_update, blocks, 256, 0, s, n, omega_, dinv, r_[l].get(), x);
       FDE_LAUNCH_CHECK();
     }
   };

@@ -10,6 +10,7 @@
 
 #include "operator.cuh"
 #include "stencil.cuh"
+#include "tail.cuh"
 #include "vec_kernels.cuh"
 
 namespace fde_b200 {
@@ -71,6 +72,7 @@ class Hierarchy {
   void cycle(size_t l, const double* b, double* x, bool zero, cudaStream_t s,
              bool prescaled = false) const;
   bool zero_guess_is_diag_scale(size_t l) const;
+  void plan_tail();
   std::vector<LevelOp> levels_;
   std::vector<std::pair<size_t, size_t>> dims_;
   std::vector<Xfer> xfer_;
@@ -82,6 +84,9 @@ class Hierarchy {
   int fuse_ = 3;
   DevBuf<double> lu_;
   DevBuf<int> perm_;
+  // levels tail_..depth-1 run as one cluster launch (tail.cuh); 0 = none
+  size_t tail_ = 0;
+  TailDesc tail_desc_{};
 };
 
 }  // namespace fde_b200

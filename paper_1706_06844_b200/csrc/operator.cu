@@ -241,6 +241,7 @@ __global__ void k_refresh(size_t n, double inv_r0, double sr0, double ax0, doubl
                           const double* __restrict__ ep, const double* __restrict__ em,
                           double* __restrict__ odp, double* __restrict__ odm,
                           double* __restrict__ diag, double* __restrict__ dinv, int* flag) {
+  pdl_enter();
   int bad = 0;
   for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < n;
        p += (size_t)gridDim.x * blockDim.x) {
@@ -277,7 +278,7 @@ void StructuredOp::refresh(const double* dp, const double* dm, const double* ep,
   for (int k = 0; k < sc.n; ++k) sc.v[k] = scales_[k];
   size_t blocks = (n + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_refresh<<<(int)blocks, 256, 0, s>>>(n, inv_r0_, s_over_r0_, ax_.first_col()[0],
+  launch_k(k_refresh, (int)blocks, 256, 0, s, n, inv_r0_, s_over_r0_, ax_.first_col()[0],
                                         ay_.first_col()[0], sc, dp, dm, ep, em, d_dp_.get(),
                                         d_dm_.get(), d_diag_.get(), dinv, flag);
   FDE_LAUNCH_CHECK();

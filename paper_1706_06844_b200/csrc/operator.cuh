@@ -68,6 +68,11 @@ class StructuredOp {
   const std::vector<double>& em() const { return em_; }
   const std::vector<double>& diagonal() const { return diag_; }
   const double* diagonal_dev() const { return d_diag_.get(); }
+  // device coefficient fields (ep/em transposed: i * n2 + j)
+  const double* dp_dev() const { return d_dp_.get(); }
+  const double* dm_dev() const { return d_dm_.get(); }
+  const double* epT_dev() const { return d_epT_.get(); }
+  const double* emT_dev() const { return d_emT_.get(); }
 
   // out = epilogue(A~ x) with A~ = apply (sign +1) or apply_rhs (sign -1).
   // Two launches (y-pass, x-pass) on stream s.  out may alias x only for

@@ -72,6 +72,7 @@ double preset_value(int kind, uint64_t key) {
 }
 
 __global__ void k_source(uint64_t seed, uint64_t m, int n1, int n2, int kind, double* v) {
+  pdl_enter();
   const size_t n = (size_t)n1 * n2;
   for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < n;
        p += (size_t)gridDim.x * blockDim.x) {
@@ -111,7 +112,7 @@ void generate_source_device(const Problem& p, const Grid& g, size_t m, double* v
   const size_t n = g.size();
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
-  k_source<<<blocks, 256, 0, s>>>(p.seed, m, (int)g.n1, (int)g.n2, p.source_kind, v);
+  launch_k(k_source, blocks, 256, 0, s, p.seed, m, (int)g.n1, (int)g.n2, p.source_kind, v);
   FDE_LAUNCH_CHECK();
 }
 

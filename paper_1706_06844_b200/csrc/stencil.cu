@@ -7,6 +7,7 @@ __global__ void k_stencil(int n1, int n2, const double* __restrict__ coef,
                           const double* __restrict__ x, double* out, int epi,
                           const double* __restrict__ b, const double* __restrict__ dinv,
                           double omega) {
+  pdl_enter();
   const size_t n = (size_t)n1 * n2;
   for (size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x; p < n;
        p += (size_t)gridDim.x * blockDim.x) {
@@ -52,7 +53,7 @@ void StencilOp::run(const double* x, double* out, int epi, const EpiArgs& e,
   const size_t n = size();
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_stencil<<<blocks, 256, 0, s>>>((int)n1_, (int)n2_, d_coef_.get(), x, out, epi, e.b, e.dinv,
+  launch_k(k_stencil, blocks, 256, 0, s, (int)n1_, (int)n2_, d_coef_.get(), x, out, epi, e.b, e.dinv,
                                    e.omega);
   FDE_LAUNCH_CHECK();
 }

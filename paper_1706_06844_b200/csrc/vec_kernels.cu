@@ -16,38 +16,47 @@ inline int blocks_for(size_t n) {
 
 __global__ void k_diag_scale(size_t n, double a, const double* __restrict__ d,
                              const double* __restrict__ b, double* __restrict__ x) {
+  pdl_enter();
   GRID_STRIDE(i, n) x[i] = a * d[i] * b[i];
 }
 __global__ void k_axpy(size_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
+  pdl_enter();
   GRID_STRIDE(i, n) y[i] = fma(a, x[i], y[i]);
 }
 __global__ void k_axpy_dev(size_t n, const double* __restrict__ a, double sgn,
                            const double* __restrict__ x, double* __restrict__ y) {
+  pdl_enter();
   const double av = sgn * *a;
   GRID_STRIDE(i, n) y[i] = fma(av, x[i], y[i]);
 }
 __global__ void k_scale_inv_dev(size_t n, const double* __restrict__ a, const double* x,
                                 double* y) {
+  pdl_enter();
   const double inv = 1.0 / *a;
   GRID_STRIDE(i, n) y[i] = x[i] * inv;
 }
 __global__ void k_jacobi_upd(size_t n, double a, const double* __restrict__ d,
                              const double* __restrict__ r, double* __restrict__ x) {
+  pdl_enter();
   GRID_STRIDE(i, n) x[i] += a * d[i] * r[i];
 }
 __global__ void k_copy_scale2(size_t n, double a, const double* __restrict__ x,
                               double* __restrict__ y) {
+  pdl_enter();
   GRID_STRIDE(i, n) y[i] = x[i] * a;
 }
 __global__ void k_scal(size_t n, double a, double* x) {
+  pdl_enter();
   GRID_STRIDE(i, n) x[i] *= a;
 }
 __global__ void k_sub(size_t n, const double* __restrict__ x, const double* __restrict__ y,
                       double* out) {
+  pdl_enter();
   GRID_STRIDE(i, n) out[i] = x[i] - y[i];
 }
 __global__ void k_lincomb(size_t n, const double* x0, const double* const* __restrict__ v,
                           const double* __restrict__ c, int k, double* out) {
+  pdl_enter();
   GRID_STRIDE(i, n) {
     double acc = x0[i];
     for (int q = 0; q < k; ++q) acc = fma(c[q], v[q][i], acc);
@@ -64,6 +73,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 __global__ void k_dot(size_t n, const double* __restrict__ x, const double* __restrict__ y,
                       double* __restrict__ partials, unsigned int* counter, double* out,
                       int sqrt_out) {
+  pdl_enter();
   __shared__ double ws[kThreads / 32];
   __shared__ bool last;
   double acc = 0.0;
@@ -171,6 +181,7 @@ __device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
 // out0 = ||w|| (sqrt of <w,w>), out1 = <v, w> in one pass over w (MGS start).
 __global__ void k_norm_dot(size_t n, const double* __restrict__ w, const double* __restrict__ v,
                            double* partials, unsigned int* counter, double* out0, double* out1) {
+  pdl_enter();
   double acc[2] = {0.0, 0.0};
   const uint64_t keep = policy_keep();
   GRID_STRIDE(i, n) {
@@ -188,6 +199,7 @@ __global__ void k_norm_dot(size_t n, const double* __restrict__ w, const double*
 __global__ void k_mgs(size_t n, double* __restrict__ w, const double* __restrict__ vk,
                       const double* __restrict__ hk, const double* vnext, double* partials,
                       unsigned int* counter, double* out, int sqrt_out) {
+  pdl_enter();
   const double h = -*hk;
   double acc[1] = {0.0};
   const bool last = vnext == w;
@@ -220,6 +232,7 @@ __global__ void k_restrict(Xfer t, const double* __restrict__ f, int f_lo,
                            double* __restrict__ c, int c_lo, int c_rows, double sc,
                            double* __restrict__ xs = nullptr,
                            const double* __restrict__ dinv = nullptr, double omega = 0.0) {
+  pdl_enter();
   const size_t nc = (size_t)t.k1 * c_rows;
   GRID_STRIDE(q, nc) {
     const int a = (int)(q % t.k1), bb = (int)(q / t.k1) + c_lo;  // global coarse row
@@ -248,6 +261,7 @@ __global__ void k_restrict(Xfer t, const double* __restrict__ f, int f_lo,
 template <bool ADD>
 __global__ void k_prolong(Xfer t, const double* __restrict__ c, int c_lo,
                           double* __restrict__ f, int f_lo, int f_rows) {
+  pdl_enter();
   const size_t nf = (size_t)t.n1 * f_rows;
   GRID_STRIDE(q, nf) {
     const int i = (int)(q % t.n1), j = (int)(q / t.n1) + f_lo;  // global fine row
@@ -263,6 +277,7 @@ struct RankOffsets {
 };
 __global__ void k_block_permute(const double* __restrict__ in, double* __restrict__ out,
                                 size_t nc, size_t d2, RankOffsets ro, int dir) {
+  pdl_enter();
   const size_t total = nc * d2;
   GRID_STRIDE(q, total) {
     const size_t c = q / d2, j = q % d2;
@@ -278,6 +293,7 @@ __global__ void k_block_permute(const double* __restrict__ in, double* __restric
 // Single-CTA forward/back substitution with a row-pivoted LU (column-major).
 __global__ void k_lu_solve(int n, const double* __restrict__ lu, const int* __restrict__ perm,
                            const double* __restrict__ b, double* __restrict__ x) {
+  pdl_enter();
   extern __shared__ double y[];
   for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = b[perm[i]];
   __syncthreads();
@@ -300,42 +316,42 @@ __global__ void k_lu_solve(int n, const double* __restrict__ lu, const int* __re
 
 void vec_diag_scale(size_t n, double a, const double* d, const double* b, double* x,
                     cudaStream_t s) {
-  k_diag_scale<<<blocks_for(n), kThreads, 0, s>>>(n, a, d, b, x);
+  launch_k(k_diag_scale, blocks_for(n), kThreads, 0, s, n, a, d, b, x);
   FDE_LAUNCH_CHECK();
 }
 void vec_axpy(size_t n, double a, const double* x, double* y, cudaStream_t s) {
-  k_axpy<<<blocks_for(n), kThreads, 0, s>>>(n, a, x, y);
+  launch_k(k_axpy, blocks_for(n), kThreads, 0, s, n, a, x, y);
   FDE_LAUNCH_CHECK();
 }
 void vec_axpy_dev(size_t n, const double* a, double sgn, const double* x, double* y,
                   cudaStream_t s) {
-  k_axpy_dev<<<blocks_for(n), kThreads, 0, s>>>(n, a, sgn, x, y);
+  launch_k(k_axpy_dev, blocks_for(n), kThreads, 0, s, n, a, sgn, x, y);
   FDE_LAUNCH_CHECK();
 }
 void vec_scale_inv_dev(size_t n, const double* a, const double* x, double* y, cudaStream_t s) {
-  k_scale_inv_dev<<<blocks_for(n), kThreads, 0, s>>>(n, a, x, y);
+  launch_k(k_scale_inv_dev, blocks_for(n), kThreads, 0, s, n, a, x, y);
   FDE_LAUNCH_CHECK();
 }
 void vec_scal(size_t n, double a, double* x, cudaStream_t s) {
-  k_scal<<<blocks_for(n), kThreads, 0, s>>>(n, a, x);
+  launch_k(k_scal, blocks_for(n), kThreads, 0, s, n, a, x);
   FDE_LAUNCH_CHECK();
 }
 void vec_jacobi_update(size_t n, double a, const double* d, const double* r, double* out,
                        cudaStream_t s) {
-  k_jacobi_upd<<<blocks_for(n), kThreads, 0, s>>>(n, a, d, r, out);
+  launch_k(k_jacobi_upd, blocks_for(n), kThreads, 0, s, n, a, d, r, out);
   FDE_LAUNCH_CHECK();
 }
 void vec_copy_scale(size_t n, double a, const double* x, double* y, cudaStream_t s) {
-  k_copy_scale2<<<blocks_for(n), kThreads, 0, s>>>(n, a, x, y);
+  launch_k(k_copy_scale2, blocks_for(n), kThreads, 0, s, n, a, x, y);
   FDE_LAUNCH_CHECK();
 }
 void vec_sub(size_t n, const double* x, const double* y, double* out, cudaStream_t s) {
-  k_sub<<<blocks_for(n), kThreads, 0, s>>>(n, x, y, out);
+  launch_k(k_sub, blocks_for(n), kThreads, 0, s, n, x, y, out);
   FDE_LAUNCH_CHECK();
 }
 void vec_lincomb(size_t n, const double* x0, const double* const* v, const double* c, int k,
                  double* out, cudaStream_t s) {
-  k_lincomb<<<blocks_for(n), kThreads, 0, s>>>(n, x0, v, c, k, out);
+  launch_k(k_lincomb, blocks_for(n), kThreads, 0, s, n, x0, v, c, k, out);
   FDE_LAUNCH_CHECK();
 }
 
@@ -344,20 +360,20 @@ Reducer::Reducer() : partials_(2 * kMaxBlocks), counter_(1) {
 }
 void Reducer::dot(size_t n, const double* x, const double* y, double* out, cudaStream_t s,
                   bool sqrt_out) {
-  k_dot<<<blocks_for(n), kThreads, 0, s>>>(n, x, y, partials_.get(), counter_.get(), out,
+  launch_k(k_dot, blocks_for(n), kThreads, 0, s, n, x, y, partials_.get(), counter_.get(), out,
                                            sqrt_out ? 1 : 0);
   FDE_LAUNCH_CHECK();
 }
 
 void Reducer::norm_dot(size_t n, const double* w, const double* v, double* norm_out,
                        double* dot_out, cudaStream_t s) {
-  k_norm_dot<<<blocks_for(n), kThreads, 0, s>>>(n, w, v, partials_.get(), counter_.get(),
+  launch_k(k_norm_dot, blocks_for(n), kThreads, 0, s, n, w, v, partials_.get(), counter_.get(),
                                                 norm_out, dot_out);
   FDE_LAUNCH_CHECK();
 }
 void Reducer::mgs(size_t n, double* w, const double* vk, const double* hk, const double* vnext,
                   double* out, bool sqrt_out, cudaStream_t s) {
-  k_mgs<<<blocks_for(n), kThreads, 0, s>>>(n, w, vk, hk, vnext, partials_.get(),
+  launch_k(k_mgs, blocks_for(n), kThreads, 0, s, n, w, vk, hk, vnext, partials_.get(),
                                            counter_.get(), out, sqrt_out ? 1 : 0);
   FDE_LAUNCH_CHECK();
 }
@@ -379,15 +395,16 @@ void xfer_restrict_rows(const Xfer& t, const double* fine, int f_lo, double* coa
                         int c_rows, double scale, cudaStream_t s) {
   const size_t nc = (size_t)t.k1 * c_rows;
   if (!nc) return;
-  k_restrict<<<blocks_for(nc), kThreads, 0, s>>>(t, fine, f_lo, coarse, c_lo, c_rows, scale);
+  launch_k(k_restrict, blocks_for(nc), kThreads, 0, s, t, fine, f_lo, coarse, c_lo, c_rows, scale,
+           (double*)nullptr, (const double*)nullptr, 0.0);
   FDE_LAUNCH_CHECK();
 }
 void xfer_prolong_rows(const Xfer& t, const double* coarse, int c_lo, double* fine, int f_lo,
                        int f_rows, bool add, cudaStream_t s) {
   const size_t nf = (size_t)t.n1 * f_rows;
   if (!nf) return;
-  if (add) k_prolong<true><<<blocks_for(nf), kThreads, 0, s>>>(t, coarse, c_lo, fine, f_lo, f_rows);
-  else k_prolong<false><<<blocks_for(nf), kThreads, 0, s>>>(t, coarse, c_lo, fine, f_lo, f_rows);
+  if (add) launch_k(k_prolong<true>, blocks_for(nf), kThreads, 0, s, t, coarse, c_lo, fine, f_lo, f_rows);
+  else launch_k(k_prolong<false>, blocks_for(nf), kThreads, 0, s, t, coarse, c_lo, fine, f_lo, f_rows);
   FDE_LAUNCH_CHECK();
 }
 void xfer_restrict(const Xfer& t, const double* fine, double* coarse, double scale,
@@ -398,7 +415,7 @@ void xfer_restrict_smooth(const Xfer& t, const double* fine, double* coarse, dou
                           const double* dinv_c, double omega, double* xc, cudaStream_t s) {
   const size_t nc = (size_t)t.k1 * t.k2;
   if (!nc) return;
-  k_restrict<<<blocks_for(nc), kThreads, 0, s>>>(t, fine, 0, coarse, 0, t.k2, scale, xc, dinv_c,
+  launch_k(k_restrict, blocks_for(nc), kThreads, 0, s, t, fine, 0, coarse, 0, t.k2, scale, xc, dinv_c,
                                                  omega);
   FDE_LAUNCH_CHECK();
 }
@@ -415,12 +432,12 @@ void block_permute(const double* in, double* out, size_t nc, size_t d2, const lo
   ro.n = nranks;
   const size_t total = nc * d2;
   if (!total) return;
-  k_block_permute<<<blocks_for(total), kThreads, 0, s>>>(in, out, nc, d2, ro, dir);
+  launch_k(k_block_permute, blocks_for(total), kThreads, 0, s, in, out, nc, d2, ro, dir);
   FDE_LAUNCH_CHECK();
 }
 void lu_solve(int n, const double* lu, const int* perm, const double* b, double* x,
               cudaStream_t s) {
-  k_lu_solve<<<1, 256, (size_t)n * sizeof(double), s>>>(n, lu, perm, b, x);
+  launch_k(k_lu_solve, 1, 256, (size_t)n * sizeof(double), s, n, lu, perm, b, x);
   FDE_LAUNCH_CHECK();
 }
 

@@ -486,19 +486,21 @@ struct PairedShape {
   static constexpr int R0 = 1 << REM;
   static constexpr int B0 = P / R0;      // butterflies per thread in the R0 stage
   static constexpr int NS0 = M / R0;     // = B0 * T
-  static constexpr int THREADS = T;
+  static constexpr int LPC = T >= 128 ? 1 : 128 / T;  // lines per CTA (lockstep)
+  static constexpr int THREADS = T * LPC;
   static constexpr int BUF = M;          // doubles per re / im plane
   // alternating exchange buffers need an even exchange count per transform
   // (both inverses start on buffer 0 with no barrier in between)
   static constexpr int NBUF = (FDE_PAIRED_DBUF && (LOGM / LP) % 2 == 0) ? 2 : 1;
-  // exchange buffer(s) + the next line's input (BUF doubles)
-  static constexpr size_t SMEM = (size_t(NBUF) * 2 + 1) * BUF * sizeof(double);
+  // per line: exchange buffer(s) + the next line's input (BUF doubles)
+  static constexpr size_t LINE_DOUBLES = (size_t(NBUF) * 2 + 1) * BUF;
+  static constexpr size_t SMEM = LPC * LINE_DOUBLES * sizeof(double);
   static constexpr int TCOLS = 8 * P;    // Qy (4P words) + Qt (4P words) per thread
   static_assert(REM != 0, "paired kernel needs a short stage");
   static constexpr int KX = LP;                 // radix-P -> radix-P exchanges
   static constexpr int KPF = 0;                 // into the paired forward stage
   static constexpr int KPI = P == 16 ? 3 : 2;   // out of the paired inverse stage
-  static_assert(T % 32 == 0 && T <= 128, "one lane quadrant per warp");
+  static_assert(T % 32 == 0 && THREADS == 128, "one lane quadrant per warp");
 };
 
 #ifndef FDE_PAIRED_MINB
@@ -813,23 +815,41 @@ struct LineIO<XPass, EPI> {
   }
 };
 
+// points per thread of the paired kernel: 16 at M = 2048; at M = 1024 either
+// 8 (one line per 128-thread CTA) or 16 (two lines per CTA, 64 threads each)
+#ifndef FDE_P16_M1024
+#define FDE_P16_M1024 0
+#endif
+template <int LOGM>
+constexpr int paired_pts() { return (LOGM >= 11 || FDE_P16_M1024) ? 16 : 8; }
+template <int LOGM>
+constexpr int paired_minb() {
+  return (LOGM >= 11 || FDE_P16_M1024) ? FDE_PAIRED_MINB : FDE_PAIRED_MINB10;
+}
+
 template <int LOGM, class Pol, int EPI>
-__global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THREADS,
-                                  LOGM >= 11 ? FDE_PAIRED_MINB : FDE_PAIRED_MINB10)
+__global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM>()>::THREADS,
+                                  paired_minb<LOGM>())
     fft_line_kernel_paired(const Pol p) {
   pdl_enter();
-  constexpr int P = LOGM >= 11 ? 16 : 8;
+  constexpr int P = paired_pts<LOGM>();
   using S = PairedShape<LOGM, P>;
   using IO = LineIO<Pol, EPI>;
   constexpr int T = S::T, H = P / 2, R0 = S::R0, B0 = S::B0, NS0 = S::NS0;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(16) double smem_all[];
+  // S::LPC lines per CTA in lockstep: thread tl of line slot ls
+  const int ls = threadIdx.x / T, tl = threadIdx.x - ls * T, warp = threadIdx.x >> 5;
+  double* const smem = smem_all + ls * S::LINE_DOUBLES;  // this line's buffers
   double* const xbuf = smem + S::NBUF * 2 * S::BUF;  // next line's input (own slots only)
   // the TMEM base address lands in the first exchange-buffer word (read into a
   // register before any exchange): no static shared memory, so four CTAs fit
   // a 196 KB carveout and the rest of the SM's L1 caches the spectral tables
-  uint32_t* const s_tbase = reinterpret_cast<uint32_t*>(smem);
-  const int tl = threadIdx.x, warp = tl >> 5;
+  uint32_t* const s_tbase = reinterpret_cast<uint32_t*>(smem_all);
   const int n = p.blk.n, nl = p.nlines();
+  constexpr int LPC = S::LPC;
+  // line of this slot in the CTA's group starting at `base` (clamped: a slot
+  // past the last line recomputes it and stores nothing)
+  auto line_of = [&](int base) { return base + ls < nl ? base + ls : nl - 1; };
 
   // Persistent CTA: lines blockIdx.x, + gridDim.x, ...  Each thread copies the
   // next line's input slots (its own positions) into xbuf while the current
@@ -854,7 +874,7 @@ __global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THRE
   }
 #endif
   if (warp == 0) tmem_alloc<S::TCOLS>(s_tbase);
-  if (blockIdx.x < nl) prefetch_x(blockIdx.x);
+  if (blockIdx.x * LPC < nl) prefetch_x(line_of(blockIdx.x * LPC));
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
@@ -866,7 +886,10 @@ __global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THRE
   const double* const ep1 = smem + S::BUF;
 
 #pragma unroll 1
-  for (int line = blockIdx.x; line < nl; line += gridDim.x) {
+  for (int base = blockIdx.x * LPC; base < nl; base += gridDim.x * LPC) {
+    const int line = line_of(base);
+    const bool live = base + ls < nl;  // uniform per line slot
+    const int next = base + gridDim.x * LPC;
     const IO io(p, line, 2 * tl);
 #if FDE_L2_PREFETCH
     for (int c = tl; c * 16 < n; c += T) p.prefetch(line, c);
@@ -881,7 +904,7 @@ __global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THRE
       v[s] = t;
       v[s + H] = make_double2(0.0, 0.0);
     }
-    if (!IO::kKeepX && line + (int)gridDim.x < nl) prefetch_x(line + gridDim.x);
+    if (!IO::kKeepX && next < nl) prefetch_x(line_of(next));
 
     // 2) forward transform; ends with this thread's paired slots in v
     double2 w1s[P];
@@ -999,12 +1022,12 @@ __global__ void __launch_bounds__(PairedShape<LOGM, (LOGM >= 11 ? 16 : 8)>::THRE
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
-        if (i0 < n) io.finish(d, ty[c].x, v[g + c].x, o[2 * c]);
-        if (i0 + 1 < n) io.finish(d + 1, ty[c].y, v[g + c].y, o[2 * c + 1]);
+        if (live && i0 < n) io.finish(d, ty[c].x, v[g + c].x, o[2 * c]);
+        if (live && i0 + 1 < n) io.finish(d + 1, ty[c].y, v[g + c].y, o[2 * c + 1]);
       }
     }
     // row pass: the next line's input lands once this line's epilogue is done
-    if (IO::kKeepX && line + (int)gridDim.x < nl) prefetch_x(line + gridDim.x);
+    if (IO::kKeepX && next < nl) prefetch_x(line_of(next));
   }
   tmem_fence_before();
   __syncthreads();
@@ -1153,7 +1176,7 @@ void launch_fft(const P& p, cudaStream_t s) {
 #endif
 template <int LOGM, class P, int EPI>
 void launch_paired_epi(const P& p, cudaStream_t s) {
-  constexpr int PP = LOGM >= 11 ? 16 : 8;
+  constexpr int PP = paired_pts<LOGM>();
   using S = PairedShape<LOGM, PP>;
   static bool configured = false;
   if (!configured) {
@@ -1185,8 +1208,8 @@ void launch_paired_epi(const P& p, cudaStream_t s) {
     per_sm = per_sm < by_tmem ? per_sm : by_tmem;
     max_ctas = sms * (per_sm > 0 ? per_sm : 1);
   }
-  const int lines = lines_of(p);
-  launch_k(fft_line_kernel_paired<LOGM, P, EPI>, lines < max_ctas ? lines : max_ctas, S::THREADS,
+  const int groups = (lines_of(p) + S::LPC - 1) / S::LPC;
+  launch_k(fft_line_kernel_paired<LOGM, P, EPI>, groups < max_ctas ? groups : max_ctas, S::THREADS,
                                          S::SMEM, s, p);
   FDE_LAUNCH_CHECK();
 }

@@ -113,3 +113,27 @@ def test_time_march_cfg1_full(cuda, orc):
         u = m.solution()
         assert it == ro["its"][k], (k, it, ro["its"][k])
         assert rel(u, ro["u_steps"][k]) <= 1e-10, (k, rel(u, ro["u_steps"][k]))
+
+
+@pytest.mark.parametrize("cfg,n,coarse", [(1, 63, 1), (1, 63, 2), (2, 255, 1), (3, 127, 1),
+                                          (3, 255, 2), (5, 255, 1), (4, 511, 1)])
+def test_vcycle_tail_matches_level_kernels(cuda, orc, monkeypatch, cfg, n, coarse):
+    """The one-launch coarse tail (csrc/tail.cu) against the per-level kernel
+    sequence on the same hierarchy plan: same V-cycle to rounding (direct vs
+    FFT Toeplitz sums), fewer launches, and both against the oracle."""
+    import torch
+    p = problem_for(cfg, steps=4)
+    b = to_dev(np.random.default_rng(n + cfg).uniform(-1, 1, n * n))
+    out = {}
+    for tail in ("1", "0"):
+        monkeypatch.setenv("FDE_MG_TAIL", tail)
+        h = fde.MgHierarchy.build_geometric(p, n, n, 4, 1, 0.7, coarse, 3)
+        h.vcycle(b)  # warm (graph-free path, per-call launches)
+        torch.cuda.synchronize()
+        k0 = fde.kernel_launches()
+        x = h.vcycle(b).cpu().numpy()
+        out[tail] = (x, fde.kernel_launches() - k0)
+    assert rel(out["1"][0], out["0"][0]) <= 1e-13, rel(out["1"][0], out["0"][0])
+    assert out["1"][1] < out["0"][1], (out["1"][1], out["0"][1])
+    xo = orc.vcycle(spec(cfg, n1=n, n2=n, steps=4, coarse=coarse), b.cpu().numpy())
+    assert rel(out["1"][0], xo) <= 1e-12

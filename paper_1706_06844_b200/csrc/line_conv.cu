@@ -818,13 +818,19 @@ struct LineIO<XPass, EPI> {
 // points per thread of the paired kernel: 16 at M = 2048; at M = 1024 either
 // 8 (one line per 128-thread CTA) or 16 (two lines per CTA, 64 threads each)
 #ifndef FDE_P16_M1024
-#define FDE_P16_M1024 0
+#define FDE_P16_M1024 1  // measured: 5-6 % faster 1023-point passes than 8 points/thread
+#endif
+#ifndef FDE_PAIRED9
+#define FDE_PAIRED9 0  // M = 512, 16 points/thread, 4 lines per CTA: measured slower (V-cycle +3 %)
+#endif
+#ifndef FDE_PAIRED8
+#define FDE_PAIRED8 0  // M = 256, 8 points/thread, 4 lines per CTA: measured slower (V-cycle +5 %)
 #endif
 template <int LOGM>
-constexpr int paired_pts() { return (LOGM >= 11 || FDE_P16_M1024) ? 16 : 8; }
+constexpr int paired_pts() { return LOGM == 8 || (LOGM == 10 && !FDE_P16_M1024) ? 8 : 16; }
 template <int LOGM>
 constexpr int paired_minb() {
-  return (LOGM >= 11 || FDE_P16_M1024) ? FDE_PAIRED_MINB : FDE_PAIRED_MINB10;
+  return paired_pts<LOGM>() == 16 ? FDE_PAIRED_MINB : FDE_PAIRED_MINB10;
 }
 
 template <int LOGM, class Pol, int EPI>
@@ -1244,8 +1250,8 @@ void launch_any(const P& p, cudaStream_t s) {
       return;
     case 6: return launch_fft<6>(p, s);
     case 7: return launch_fft<7>(p, s);
-    case 8: return launch_fft<8>(p, s);
-    case 9: return launch_fft<9>(p, s);
+    case 8: return FDE_PAIRED8 ? launch_paired<8>(p, s) : launch_fft<8>(p, s);
+    case 9: return FDE_PAIRED9 ? launch_paired<9>(p, s) : launch_fft<9>(p, s);
     case 10: return FDE_PAIRED ? launch_paired<10>(p, s) : launch_fft<10>(p, s);
     case 11: return FDE_PAIRED ? launch_paired<11>(p, s) : launch_fft<11>(p, s);
     case 12: return launch_fft<12>(p, s);

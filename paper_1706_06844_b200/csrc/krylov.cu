@@ -267,17 +267,25 @@ KrylovResult KrylovWorkspace::gmres(const StructuredOp& a, const Precond* m,
     for (size_t i = 0; i < rst && !cycle_done; ++i) {
       a.apply(v_[i].get(), t_.get(), s);
       precondition(m, t_.get(), w_.get(), s);
-      // modified Gram-Schmidt (krylov.cpp:92-97), each subtraction fused with
-      // the next projection: i + 2 passes over w instead of 2 (i + 1) + 2
-      red_.norm_dot(n, w_.get(), v_[0].get(), dnorm0, dh, s);
-      for (size_t k = 0; k <= i; ++k)
-        red_.mgs(n, w_.get(), v_[k].get(), dh + k, k < i ? v_[k + 1].get() : w_.get(),
-                 k < i ? dh + k + 1 : dnrmw, k == i, s);
+      // modified Gram-Schmidt (krylov.cpp:92-97): one cooperative launch with
+      // w resident in shared memory (and v_{i+1} = w / ||w|| formed on the
+      // way out), else each subtraction fused with the next projection: i + 2
+      // passes over w instead of 2 (i + 1) + 2
+      const bool chained = red_.mgs_chain(n, w_.get(), dptr_.get(), (int)i, dh, dnorm0, dnrmw,
+                                          v_[i + 1].get(), s);
+      if (!chained) {
+        red_.norm_dot(n, w_.get(), v_[0].get(), dnorm0, dh, s);
+        for (size_t k = 0; k <= i; ++k)
+          red_.mgs(n, w_.get(), v_[k].get(), dh + k, k < i ? v_[k + 1].get() : w_.get(),
+                   k < i ? dh + k + 1 : dnrmw, k == i, s);
+      }
       fetch(ld + 2, s);
       for (size_t k = 0; k <= i; ++k) h[i * ld + k] = hsc_[k];
       const double norm0 = hsc_[ld];
       double hip = hsc_[ld + 1];
+      bool reorth = false;
       if (hip < 1e-8 * norm0) {  // second pass (krylov.cpp:98-104)
+        reorth = true;
         red_.dot(n, v_[0].get(), w_.get(), dreo, s);
         for (size_t k = 0; k <= i; ++k)
           red_.mgs(n, w_.get(), v_[k].get(), dreo + k, k < i ? v_[k + 1].get() : w_.get(),
@@ -304,7 +312,8 @@ KrylovResult KrylovWorkspace::gmres(const StructuredOp& a, const Precond* m,
       spanned = i + 1;
       const double est = std::fabs(g[i + 1]) / norm_b;
       res.residual_history.push_back(est);
-      if (!happy) copy_scale(n, 1.0 / hip, w_.get(), v_[i + 1].get(), s);
+      // (the chained Gram-Schmidt already formed v_{i+1} unless a second pass ran)
+      if (!happy && (!chained || reorth)) copy_scale(n, 1.0 / hip, w_.get(), v_[i + 1].get(), s);
 
       if (est <= cfg.tol || happy) {  // verify the estimate (krylov.cpp:132-149)
         y = back_substitute(h, ld, g, spanned);

@@ -1,3 +1,4 @@
+#include <cstdlib>
 #include "vec_kernels.cuh"
 
 namespace fde_b200 {
@@ -178,6 +179,13 @@ __device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
 
+__device__ __forceinline__ double2 ld2_hint(const double* p, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+
 // out0 = ||w|| (sqrt of <w,w>), out1 = <v, w> in one pass over w (MGS start).
 __global__ void k_norm_dot(size_t n, const double* __restrict__ w, const double* __restrict__ v,
                            double* partials, unsigned int* counter, double* out0, double* out1) {
@@ -268,6 +276,175 @@ __global__ void k_prolong(Xfer t, const double* __restrict__ c, int c_lo,
     const double v = prolong_point(t, c, c_lo, i, j);
     if (ADD) f[q] += v;
     else f[q] = v;
+  }
+}
+
+// ---- the whole modified Gram-Schmidt of one GMRES iteration, one launch ----
+// Cooperative grid of one 1024-thread CTA per SM; CTA b keeps its slice of w
+// in shared memory for the whole chain, so a projection pass streams only the
+// basis vectors (v_{k+1} from HBM, v_k again from L2) instead of reading and
+// writing w every pass.  Same per-element arithmetic as k_norm_dot / k_mgs /
+// k_copy_scale; the grid-wide sums combine per-CTA partials in CTA order
+// (deterministic, identical in every CTA).
+constexpr int kChainThreads = 1024;
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// all CTAs of the (co-resident) grid reach the barrier; *bar counts arrivals
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (ld_acquire_u32(bar) < target) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kChainThreads, 1)
+    k_mgs_chain(size_t n, size_t chunk, double* __restrict__ w, const double* const* __restrict__ v,
+                int last, double* dh, double* dnorm0, double* dnrmw, double* __restrict__ vout,
+                double* partials, unsigned int* bar) {
+  extern __shared__ __align__(16) double ws[];  // this CTA's slice of w
+  __shared__ double red[2][kChainThreads / 32];
+  __shared__ double sums[2];
+  const size_t lo = blockIdx.x * chunk;
+  const int cnt = lo < n ? (int)((n - lo < chunk) ? n - lo : chunk) : 0;
+  const uint64_t keep = policy_keep(), stream = policy_stream();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned phase = 0;
+  // grid-wide sums of (a, b): per-CTA partials (double-buffered by phase
+  // parity), one barrier, then every CTA adds them in CTA order
+  auto grid_sum = [&](double a, double b) {
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) {
+      red[0][warp] = a;
+      red[1][warp] = b;
+    }
+    __syncthreads();
+    double* const part = partials + (phase & 1) * 2 * gridDim.x;
+    if (threadIdx.x == 0) {
+      double ta = 0.0, tb = 0.0;
+      for (int k = 0; k < kChainThreads / 32; ++k) {
+        ta += red[0][k];
+        tb += red[1][k];
+      }
+      part[2 * blockIdx.x] = ta;
+      part[2 * blockIdx.x + 1] = tb;
+    }
+    ++phase;
+    grid_barrier(bar, phase * gridDim.x);
+    if (warp == 0) {
+      double ta = 0.0, tb = 0.0;
+      for (int k = lane; k < (int)gridDim.x; k += 32) {
+        ta += __ldcg(part + 2 * k);
+        tb += __ldcg(part + 2 * k + 1);
+      }
+      ta = warp_sum(ta);
+      tb = warp_sum(tb);
+      if (lane == 0) {
+        sums[0] = ta;
+        sums[1] = tb;
+      }
+    }
+    __syncthreads();
+  };
+
+  // pairs of elements (16-byte loads; the slice start is even), plus the odd
+  // last element of the last slice
+  double2* const ws2 = reinterpret_cast<double2*>(ws);
+  const int pairs = cnt >> 1, tail = (cnt & 1) ? cnt - 1 : -1;
+  // ||w|| and <w, v_0> while w moves into shared memory (k_norm_dot)
+  {
+    const double* v0 = v[0] + lo;
+    const double* wg = w + lo;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < pairs; e += kChainThreads) {
+      const double2 wi = ld2_hint(wg + 2 * e, stream), vi = ld2_hint(v0 + 2 * e, keep);
+      ws2[e] = wi;
+      a0 = fma(wi.x, wi.x, a0);
+      a1 = fma(vi.x, wi.x, a1);
+      a0 = fma(wi.y, wi.y, a0);
+      a1 = fma(vi.y, wi.y, a1);
+    }
+    if (threadIdx.x == 0 && tail >= 0) {
+      const double wi = wg[tail];
+      ws[tail] = wi;
+      a0 = fma(wi, wi, a0);
+      a1 = fma(v0[tail], wi, a1);
+    }
+    grid_sum(a0, a1);
+  }
+  const double norm0 = sqrt(sums[0]);
+  double h = sums[1];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *dnorm0 = norm0;
+    dh[0] = h;
+  }
+  double hip = 0.0;
+  // w -= h_k v_k fused with <v_{k+1}, w> (k_mgs); the last pass forms ||w||
+  for (int k = 0; k <= last; ++k) {
+    const double* vk = v[k] + lo;
+    const double* vn = k < last ? v[k + 1] + lo : nullptr;
+    const double nh = -h;
+    double acc = 0.0;
+    __syncthreads();  // sums[] is rewritten by this pass's reduction
+    if (vn) {
+#pragma unroll 4
+      for (int e = threadIdx.x; e < pairs; e += kChainThreads) {
+        const double2 a = ld2_hint(vk + 2 * e, stream), b = ld2_hint(vn + 2 * e, keep);
+        double2 wi = ws2[e];
+        wi.x = fma(nh, a.x, wi.x);
+        wi.y = fma(nh, a.y, wi.y);
+        ws2[e] = wi;
+        acc = fma(b.x, wi.x, acc);
+        acc = fma(b.y, wi.y, acc);
+      }
+    } else {
+#pragma unroll 4
+      for (int e = threadIdx.x; e < pairs; e += kChainThreads) {
+        const double2 a = ld2_hint(vk + 2 * e, stream);
+        double2 wi = ws2[e];
+        wi.x = fma(nh, a.x, wi.x);
+        wi.y = fma(nh, a.y, wi.y);
+        ws2[e] = wi;
+        acc = fma(wi.x, wi.x, acc);
+        acc = fma(wi.y, wi.y, acc);
+      }
+    }
+    if (threadIdx.x == 0 && tail >= 0) {
+      const double wi = fma(nh, vk[tail], ws[tail]);
+      ws[tail] = wi;
+      acc = fma(vn ? vn[tail] : wi, wi, acc);
+    }
+    grid_sum(acc, 0.0);
+    if (k < last) {
+      h = sums[0];
+      if (blockIdx.x == 0 && threadIdx.x == 0) dh[k + 1] = h;
+    } else {
+      hip = sqrt(sums[0]);
+      if (blockIdx.x == 0 && threadIdx.x == 0) *dnrmw = hip;
+    }
+  }
+  // v_{i+1} = w (1 / ||w||) (copy_scale, krylov.cpp:127-130); a second
+  // Gram-Schmidt pass (hip < 1e-8 norm0, krylov.cpp:98-104) needs w itself
+  if (hip < 1e-8 * norm0) {
+    for (int e = threadIdx.x; e < cnt; e += kChainThreads) w[lo + e] = ws[e];
+  } else {
+    const double a = 1.0 / hip;
+    double2* const out2 = reinterpret_cast<double2*>(vout + lo);
+    for (int e = threadIdx.x; e < pairs; e += kChainThreads) {
+      const double2 wi = ws2[e];
+      out2[e] = make_double2(wi.x * a, wi.y * a);
+    }
+    if (threadIdx.x == 0 && tail >= 0) vout[lo + tail] = ws[tail] * a;
   }
 }
 
@@ -371,6 +548,53 @@ void Reducer::norm_dot(size_t n, const double* w, const double* v, double* norm_
                                                 norm_out, dot_out);
   FDE_LAUNCH_CHECK();
 }
+bool Reducer::mgs_chain(size_t n, double* w, const double* const* v_dev, int last, double* dh,
+                        double* dnorm0, double* dnrmw, double* vout, cudaStream_t s) {
+  static int grid = -1;
+  static size_t max_smem = 0;
+  if (grid < 0) {
+    grid = 0;
+    int dev = 0, sms = 0, coop = 0, optin = 0;
+    FDE_CUDA(cudaGetDevice(&dev));
+    FDE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FDE_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    FDE_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (const char* e = std::getenv("FDE_MGS_CHAIN"))
+      if (e[0] == '0') coop = 0;
+    if (coop) {
+      cudaFuncAttributes fa{};
+      FDE_CUDA(cudaFuncGetAttributes(&fa, k_mgs_chain));
+      max_smem = (size_t)optin - fa.sharedSizeBytes;
+      FDE_CUDA(cudaFuncSetAttribute(k_mgs_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)max_smem));
+      grid = sms;
+    }
+  }
+  if (grid == 0) return false;
+  const size_t chunk = ((n + grid - 1) / grid + 1) & ~size_t(1);
+  if (chunk * sizeof(double) > max_smem) return false;
+  if (chain_partials_.size() == 0) {
+    chain_partials_.alloc(4 * (size_t)grid);
+    chain_bar_.alloc(1);
+  }
+  FDE_CUDA(cudaMemsetAsync(chain_bar_.get(), 0, sizeof(unsigned int), s));
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kChainThreads);
+  cfg.dynamicSmemBytes = chunk * sizeof(double);
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cuda_check(cudaLaunchKernelEx(&cfg, k_mgs_chain, n, chunk, w, v_dev, last, dh, dnorm0, dnrmw,
+                                vout, chain_partials_.get(), chain_bar_.get()),
+             "kernel launch");
+  FDE_LAUNCH_CHECK();
+  return true;
+}
+
 void Reducer::mgs(size_t n, double* w, const double* vk, const double* hk, const double* vnext,
                   double* out, bool sqrt_out, cudaStream_t s) {
   launch_k(k_mgs, blocks_for(n), kThreads, 0, s, n, w, vk, hk, vnext, partials_.get(),

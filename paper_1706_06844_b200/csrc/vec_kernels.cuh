@@ -45,10 +45,20 @@ class Reducer {
   // w -= (*hk) v_k, then *out = <v_next, w> (sqrt when sqrt_out; v_next may be w)
   void mgs(size_t n, double* w, const double* vk, const double* hk, const double* vnext,
            double* out, bool sqrt_out, cudaStream_t s);
+  // The whole Gram-Schmidt of GMRES iteration `last` (krylov.cpp:92-97,
+  // 127-130) in one cooperative launch: *dnorm0 = ||w||, dh[k] = <w_k, v_k>
+  // with w_{k+1} = w_k - dh[k] v_k for k <= last, *dnrmw = ||w_{last+1}||, and
+  // vout = w_{last+1} / *dnrmw -- or, when *dnrmw < 1e-8 *dnorm0 (a second
+  // pass follows), w_{last+1} written back to w.  False (nothing launched)
+  // when w does not fit the SMs' shared memory or cooperative launch is off.
+  bool mgs_chain(size_t n, double* w, const double* const* v_dev, int last, double* dh,
+                 double* dnorm0, double* dnrmw, double* vout, cudaStream_t s);
 
  private:
   DevBuf<double> partials_;
   DevBuf<unsigned int> counter_;
+  DevBuf<double> chain_partials_;
+  DevBuf<unsigned int> chain_bar_;
 };
 
 Xfer make_xfer(int n1, int n2, bool cx, bool cy);

@@ -83,7 +83,8 @@ def test_solve_matches_reference(cuda, ref, cli, tmp_path, example, n, precond):
     ro = ref.time_march(s)
     assert avg == f"{np.mean(ro['its']):.3f}"
     e_ref = ref.error_inf(s, ro["u"], 1.0)
-    assert abs(float(err) - e_ref) <= 1e-9 * e_ref + 1e-15, (err, e_ref)
+    # equal at the CSV's printed precision (report.cpp:66-70: %.5e)
+    assert abs(float(err) - e_ref) <= 5e-6 * e_ref, (err, e_ref)
     assert man["command"] == "solve" and man["parameters"]["n"] == str(n)
     assert man["parameters"]["precond"] == precond and man["parameters"]["m"] == str(n)
 

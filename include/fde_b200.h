@@ -155,7 +155,11 @@ int fde_mg_destroy(fde_mg h);
 
 /* ------------------------------------------------------ preconditioner
  * make_preconditioner (proj/include/fde/precond.hpp:94-98): kind 0 none,
- * 1 p2 (banded Galerkin V-cycle), 2 mgm (geometric V-cycle). */
+ * 1 p2 (banded Galerkin V-cycle), 2 mgm (geometric V-cycle), 3 p2-exact
+ * (exact banded solve with the order-2 companion, P2ExactPrecond), 4
+ * mgm-galerkin (Galerkin R A P levels of the full operator, n1, n2 <= 128,
+ * MgmGalerkinPrecond; p must be given).  The reference numbers its enum
+ * none, p2, p2_exact, mgm, mgm_galerkin (precond.hpp:18). */
 typedef struct fde_precond_s* fde_precond;
 int fde_precond_create(int kind, const fde_problem* p, size_t n1, size_t n2, size_t steps,
                        size_t m, fde_op op, double omega, size_t cycles, int coarse,
@@ -190,7 +194,7 @@ int fde_bicgstab(fde_op a, fde_precond m, const fde_solver_config* cfg, const do
 /* ----------------------------------------------------------- time march
  * DriverConfig (proj/include/fde/driver.hpp:12-21) + solver choice. */
 typedef struct {
-  int precond;          /* 0 none, 1 p2, 2 mgm */
+  int precond;          /* 0 none, 1 p2, 2 mgm, 3 p2-exact, 4 mgm-galerkin */
   double tol;
   size_t restart;
   size_t max_outer;

@@ -290,8 +290,13 @@ int ref_time_march(const ref_spec* s, double* u_out, int* its, double* res, doub
     const Setup st = make_setup(*s);
     if (st.pq != 0) throw std::invalid_argument("time_march supports (p,q)=(1,0) only");
     fde::DriverConfig c;
-    c.precond = s->precond == 2 ? fde::PrecondKind::mgm
-                                : (s->precond == 1 ? fde::PrecondKind::p2 : fde::PrecondKind::none);
+    {
+      const fde::PrecondKind kinds[] = {fde::PrecondKind::none, fde::PrecondKind::p2,
+                                        fde::PrecondKind::mgm, fde::PrecondKind::p2_exact,
+                                        fde::PrecondKind::mgm_galerkin};
+      if (s->precond < 0 || s->precond > 4) throw std::invalid_argument("precond kind");
+      c.precond = kinds[s->precond];
+    }
     c.tol = s->tol;
     c.restart = static_cast<std::size_t>(s->restart);
     c.max_outer = static_cast<std::size_t>(s->max_outer);

@@ -27,7 +27,7 @@ struct ref_spec {
   int cfg;            // 1..5 (BASELINE configs), or 0 = cfg1 fields with pq/alpha overrides
   int n1, n2;         // grid (0 = config default)
   int steps;          // time steps (0 = config default)
-  int precond;        // 0 none, 1 p2, 2 mgm
+  int precond;        // 0 none, 1 p2, 2 mgm, 3 p2-exact, 4 mgm-galerkin
   int restart;        // GMRES restart
   int max_outer;
   int cycles;         // V-cycles per preconditioner apply
@@ -278,6 +278,13 @@ inline std::unique_ptr<fde::Precond> make_pc(const ref_spec& s, const Setup& st,
   if (s.precond == 1)
     return fde::make_preconditioner(fde::PrecondKind::p2, st.p, st.g, 1, op, s.omega,
                                     static_cast<std::size_t>(s.cycles));
+  if (s.precond == 3)
+    return fde::make_preconditioner(fde::PrecondKind::p2_exact, st.p, st.g, 1, op, s.omega,
+                                    static_cast<std::size_t>(s.cycles));
+  if (s.precond == 4)
+    return fde::make_preconditioner(fde::PrecondKind::mgm_galerkin, st.p, st.g, 1, op, s.omega,
+                                    static_cast<std::size_t>(s.cycles), coarse_of(s.coarse),
+                                    static_cast<std::size_t>(s.coarse_sweeps));
   return nullptr;
 }
 

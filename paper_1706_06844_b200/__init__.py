@@ -29,13 +29,15 @@ __all__ = [
     "StructuredFdeOperator", "MgHierarchy", "Preconditioner", "make_preconditioner",
     "SolverConfig", "KrylovResult", "gmres", "bicgstab", "DriverConfig", "March",
     "SolveReport", "time_march", "plan_level_dims", "transfer", "kernel_launches",
-    "PRECOND_NONE", "PRECOND_P2", "PRECOND_MGM", "COARSE_LU", "COARSE_SWEEPS", "COARSE_NONE",
+    "PRECOND_NONE", "PRECOND_P2", "PRECOND_MGM", "PRECOND_P2_EXACT", "PRECOND_MGM_GALERKIN",
+    "COARSE_LU", "COARSE_SWEEPS", "COARSE_NONE",
 ]
 
 PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = PKG_DIR / "libfde_b200.so"
 
 PRECOND_NONE, PRECOND_P2, PRECOND_MGM = 0, 1, 2
+PRECOND_P2_EXACT, PRECOND_MGM_GALERKIN = 3, 4  # precond.cpp:90-133 (oracle-size variants)
 COARSE_LU, COARSE_SWEEPS, COARSE_NONE = 0, 1, 2
 
 _c_size = ctypes.c_size_t
@@ -509,7 +511,8 @@ class Preconditioner:
 
 def make_preconditioner(kind, problem, n1, n2, steps, m, op, omega, cycles=1,
                         coarse=COARSE_SWEEPS, coarse_sweeps=3) -> Preconditioner:
-    """make_preconditioner (precond.hpp:94-98); kind 0 none, 1 p2, 2 mgm."""
+    """make_preconditioner (precond.hpp:94-98); kind 0 none, 1 p2, 2 mgm, 3 p2-exact,
+    4 mgm-galerkin (the problem is needed for 2 and 4)."""
     h = _c_vp()
     s = problem.c_struct() if problem is not None else None
     _check(load_library().fde_precond_create(kind, ctypes.byref(s) if s is not None else None, n1, n2,

@@ -183,6 +183,16 @@ std::shared_ptr<Precond> make_pc(int kind, const Problem& p, const Grid& g, size
     case PC_MGM:
       return std::make_shared<Precond>(
           PC_MGM, build_geometric_hierarchy(p, g, m, omega, coarse, sweeps), op->size(), cycles);
+    case PC_P2_EXACT:
+      return std::make_shared<Precond>(
+          std::make_shared<BandedLu>(build_p2_csr(*op), op->n1()), op->size());
+    case PC_MGM_GALERKIN: {  // precond.cpp:150-155
+      const auto plan = plan_level_dims(op->n1(), op->n2(), anisotropy_ratio(*op, p.alpha, p.beta),
+                                        p.alpha, p.beta);
+      return std::make_shared<Precond>(
+          PC_MGM_GALERKIN, build_galerkin_csr_hierarchy(*op, plan, omega, coarse, sweeps),
+          op->size(), cycles);
+    }
   }
   throw InvalidArgument("unknown preconditioner kind");
 }
@@ -487,7 +497,8 @@ int fde_precond_create(int kind, const fde_problem* p, size_t n1, size_t n2, siz
   return guard([&] {
     need(out && op, "null argument");
     auto h = std::make_unique<fde_precond_s>();
-    if (kind == PC_MGM) {
+    if (kind == PC_MGM || kind == PC_MGM_GALERKIN) {
+      need(p != nullptr, "this preconditioner needs the problem");
       const Problem pr = to_problem(p);
       const Grid g(pr, n1, n2, steps);
       h->pc = make_pc(kind, pr, g, m, op->op, omega, cycles, coarse, coarse_sweeps);
@@ -594,8 +605,8 @@ int fde_march_step(fde_march h, const double* source, int source_mode, void* str
         if (!refresh_geometric_hierarchy(*hh, h->p, h->g, m, h->fields, s))
           h->pc = make_pc(kind, h->p, h->g, m, h->next, h->cfg.omega, h->cfg.cycles,
                           h->cfg.coarse, h->cfg.coarse_sweeps);  // the level plan moved
-      } else if (kind == PC_P2) {
-        h->next->sync_host(s);  // build_p2 reads the operator's fields
+      } else if (kind == PC_P2 || kind == PC_P2_EXACT || kind == PC_MGM_GALERKIN) {
+        h->next->sync_host(s);  // build_p2 / to_csr read the operator's fields
         h->pc = make_pc(kind, h->p, h->g, m, h->next, h->cfg.omega, h->cfg.cycles,
                         h->cfg.coarse, h->cfg.coarse_sweeps);
       }

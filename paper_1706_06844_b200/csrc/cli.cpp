@@ -8,9 +8,8 @@
 // Same flags, defaults, CSV columns and manifest as the reference; the
 // reference's `--n <= 4096` cap becomes the line-kernel limit (n <= 4096 per
 // direction).  Extensions: --config K runs BASELINE configuration K (1..5,
-// seeded sources), --solver bicgstab, --seed.  The Galerkin
-// variants `p2-exact` / `mgm-galerkin` are not part of the B200 build (their
-// table columns read "n/a").  Exit codes follow the reference: 0 ok, 1 some
+// seeded sources), --solver bicgstab, --seed.  Exit codes
+// follow the reference: 0 ok, 1 some
 // step did not converge, 2 usage error; library failures print
 // fde_last_error() and exit 3.
 #include <algorithm>
@@ -143,8 +142,8 @@ int precond_id(const std::string& name) {
   if (name == "none") return 0;
   if (name == "p2") return 1;
   if (name == "mgm") return 2;
-  if (name == "p2-exact" || name == "mgm-galerkin")
-    throw Usage("--precond " + name + " is not part of the B200 build (see DESIGN.md 9)");
+  if (name == "p2-exact") return 3;
+  if (name == "mgm-galerkin") return 4;
   throw Usage("unknown preconditioner: " + name);
 }
 int coarse_id(const std::string& name) {  // cli.cpp:61-66
@@ -332,10 +331,6 @@ int cmd_table(Args& a) {  // cli.cpp:151-211
       std::vector<std::string> cells{std::to_string(n)};
       double err = std::numeric_limits<double>::quiet_NaN();
       for (const auto& c : columns) {
-        if (c == "p2-exact" || c == "mgm-galerkin") {
-          cells.push_back("n/a");
-          continue;
-        }
         fde_driver_config cfg;
         fde_driver_config_default(&cfg);
         cfg.precond = precond_id(c);
@@ -370,7 +365,8 @@ int cmd_table(Args& a) {  // cli.cpp:151-211
 
 const char* kHelp =
     "fde_b200 -- B200 fractional diffusion solver (drop-in for `fde solve` / `fde table`)\n"
-    "  solve (--example K | --coeff-preset K | --config K) --n N [--m M] [--precond none|p2|mgm]\n"
+    "  solve (--example K | --coeff-preset K | --config K) --n N [--m M]\n"
+    "        [--precond none|p2|p2-exact|mgm|mgm-galerkin]\n"
     "        [--tol T] [--restart R] [--max-outer O] [--omega W] [--vcycles-per-apply C]\n"
     "        [--coarse lu|sweeps|none] [--coarse-sweeps S] [--alpha A] [--beta B]\n"
     "        [--domain ax bx ay by] [--solver gmres|bicgstab] [--seed S] [--out-dir DIR]\n"

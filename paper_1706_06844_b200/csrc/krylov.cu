@@ -100,6 +100,11 @@ Precond::Precond(int kind, std::shared_ptr<Hierarchy> h, size_t n, size_t cycles
   if (const char* e = std::getenv("FDE_NO_GRAPH")) use_graphs_ = e[0] != '1';
 }
 
+Precond::Precond(std::shared_ptr<BandedLu> lu, size_t n)
+    : kind_(PC_P2_EXACT), lu_(std::move(lu)), n_(n), cycles_(1) {
+  if (!lu_ || lu_->size() != n_) throw InvalidArgument("p2-exact needs its factorisation");
+}
+
 Precond::~Precond() {
   for (Entry& e : graphs_) cudaGraphExecDestroy(e.exec);
   if (cap_) cudaStreamDestroy(cap_);
@@ -117,6 +122,10 @@ void Precond::record(const double* r, double* z, cudaStream_t s) const {
 void Precond::apply(const double* r, double* z, cudaStream_t s) const {
   if (kind_ == PC_NONE) {
     copy_vec(n_, r, z, s);
+    return;
+  }
+  if (kind_ == PC_P2_EXACT) {
+    lu_->solve(r, z, s);
     return;
   }
   if (!use_graphs_) {

@@ -16,11 +16,15 @@
 
 namespace fde_b200 {
 
-enum PrecondKind : int { PC_NONE = 0, PC_P2 = 1, PC_MGM = 2 };
+// PrecondKind (precond.hpp:18); numbering of the C ABI (p2-exact and
+// mgm-galerkin appended after the reference's default kinds)
+enum PrecondKind : int { PC_NONE = 0, PC_P2 = 1, PC_MGM = 2, PC_P2_EXACT = 3, PC_MGM_GALERKIN = 4 };
 
 class Precond {
  public:
   Precond(int kind, std::shared_ptr<Hierarchy> h, size_t n, size_t cycles);
+  // PC_P2_EXACT: the exact banded solve (P2ExactPrecond, precond.cpp:90-101)
+  Precond(std::shared_ptr<BandedLu> lu, size_t n);
   ~Precond();
   Precond(const Precond&) = delete;
   Precond& operator=(const Precond&) = delete;
@@ -38,6 +42,7 @@ class Precond {
   void record(const double* r, double* z, cudaStream_t s) const;
   int kind_;
   std::shared_ptr<Hierarchy> h_;
+  std::shared_ptr<BandedLu> lu_;
   size_t n_, cycles_;
   bool use_graphs_ = true;
   mutable cudaStream_t cap_ = nullptr;

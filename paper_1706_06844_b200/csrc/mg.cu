@@ -83,6 +83,10 @@ std::vector<double> dense_of(const LevelOp& op, size_t n1, size_t n2) {
           at(p, i + jj * n1) += o.s_over_r() * (o.ep()[p] * o.block_y().entry(j, jj) +
                                                 o.em()[p] * o.block_y().entry(jj, j));
       }
+  } else if (op.csr) {
+    const Csr& c = op.csr->matrix();
+    for (size_t r = 0; r < n; ++r)
+      for (uint32_t k = c.ptr[r]; k < c.ptr[r + 1]; ++k) at(r, c.idx[k]) = c.val[k];
   } else {
     const std::vector<double>& c = op.stencil->coef();
     for (size_t j = 0; j < n2; ++j)

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "operator.cuh"
+#include "csr.cuh"
 #include "stencil.cuh"
 #include "tail.cuh"
 #include "vec_kernels.cuh"
@@ -30,16 +31,21 @@ std::vector<std::pair<size_t, size_t>> plan_level_dims(size_t n1, size_t n2, dou
 // multigrid.cpp:98-110 (full coarsening down to <= 8 x 8, Galerkin default)
 std::vector<std::pair<size_t, size_t>> level_dims(size_t n1, size_t n2);
 
-// A level operator: either the structured (diag x Toeplitz) operator or a
-// Galerkin 9-point stencil (P2 path).
+// A level operator: the structured (diag x Toeplitz) operator, a Galerkin
+// 9-point stencil (P2 path) or a CSR matrix (Galerkin levels on the full
+// operator, `mgm-galerkin`).
 struct LevelOp {
   std::shared_ptr<StructuredOp> sop;
   std::shared_ptr<StencilOp> stencil;
-  size_t size() const { return sop ? sop->size() : stencil->size(); }
-  const std::vector<double>& diagonal() const { return sop ? sop->diagonal() : stencil->diagonal(); }
+  std::shared_ptr<CsrOp> csr;
+  size_t size() const { return sop ? sop->size() : stencil ? stencil->size() : csr->size(); }
+  const std::vector<double>& diagonal() const {
+    return sop ? sop->diagonal() : stencil ? stencil->diagonal() : csr->diagonal();
+  }
   void run(const double* x, double* out, int epi, const EpiArgs& e, cudaStream_t s) const {
     if (sop) sop->run(x, out, 1.0, epi, e, s);
-    else stencil->run(x, out, epi, e, s);
+    else if (stencil) stencil->run(x, out, epi, e, s);
+    else csr->run(x, out, epi, e, s);
   }
 };
 

@@ -233,6 +233,48 @@ std::shared_ptr<Hierarchy> build_p2_hierarchy(const StructuredOp& op, double ome
                                      3);
 }
 
+Csr build_p2_csr(const StructuredOp& op) {
+  const size_t n1 = op.n1(), n2 = op.n2(), n = n1 * n2;
+  std::vector<Csr::Triplet> t;
+  t.reserve(5 * n);
+  for (size_t j = 0; j < n2; ++j)
+    for (size_t i = 0; i < n1; ++i) {  // precond.cpp:50-73
+      const uint32_t p = (uint32_t)(i + j * n1);
+      const double cx = op.dp()[p] + op.dm()[p];
+      const double cy = op.s_over_r() * (op.ep()[p] + op.em()[p]);
+      t.push_back({p, p, op.inv_r() + 2.0 * cx + 2.0 * cy});
+      if (i > 0) t.push_back({p, p - 1, -cx});
+      if (i + 1 < n1) t.push_back({p, p + 1, -cx});
+      if (j > 0) t.push_back({p, (uint32_t)(p - n1), -cy});
+      if (j + 1 < n2) t.push_back({p, (uint32_t)(p + n1), -cy});
+    }
+  return Csr::from_triplets(n, n, std::move(t));
+}
+
+std::shared_ptr<Hierarchy> build_galerkin_csr_hierarchy(const StructuredOp& op,
+                                                        std::vector<std::pair<size_t, size_t>> dims,
+                                                        double omega, int coarse,
+                                                        size_t coarse_sweeps) {
+  if (op.n1() > 128 || op.n2() > 128)
+    throw InvalidArgument("galerkin variant limited to 128 x 128 grids");  // precond.cpp:121-123
+  if (dims.empty() || dims.front() != std::make_pair(op.n1(), op.n2()))
+    throw InvalidArgument("plan does not start at the fine grid");
+  Csr a = structured_to_csr(op);
+  std::vector<LevelOp> levels;
+  for (size_t l = 0; l < dims.size(); ++l) {
+    if (l > 0)
+      a = rap(prolong_matrix(make_xfer((int)dims[l - 1].first, (int)dims[l - 1].second,
+                                       dims[l].first < dims[l - 1].first,
+                                       dims[l].second < dims[l - 1].second)),
+              a);
+    LevelOp lev;
+    lev.csr = std::make_shared<CsrOp>(a);
+    levels.push_back(std::move(lev));
+  }
+  return std::make_shared<Hierarchy>(std::move(levels), dims, MODE_GALERKIN, omega, coarse,
+                                     coarse_sweeps);
+}
+
 ExampleSpec make_example_spec(int which, double alpha, double beta, double ax, double bx,
                               double ay, double by) {
   if (which < 1 || which > 3) throw InvalidArgument("example index must be 1..3");

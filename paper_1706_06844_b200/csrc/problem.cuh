@@ -59,6 +59,15 @@ std::shared_ptr<Hierarchy> build_geometric_hierarchy(const Problem& p, const Gri
 // P2VcyclePrecond hierarchy: build_p2 (precond.cpp:50-73) + Galerkin R A P
 // levels (multigrid.cpp:443-475), coarsest CoarseSolve::none.
 std::shared_ptr<Hierarchy> build_p2_hierarchy(const StructuredOp& fine, double omega);
+// build_p2 as CSR (5-point, precond.cpp:50-73), for the exact banded solve
+Csr build_p2_csr(const StructuredOp& op);
+// build_galerkin_hierarchy on the full operator (MgmGalerkinPrecond,
+// precond.cpp:115-133, multigrid.cpp:443-475): CSR(M) and R A P coarse
+// levels over the given plan; the reference limits it to 128 x 128 grids.
+std::shared_ptr<Hierarchy> build_galerkin_csr_hierarchy(const StructuredOp& fine,
+                                                        std::vector<std::pair<size_t, size_t>> plan,
+                                                        double omega, int coarse,
+                                                        size_t coarse_sweeps);
 
 // make_example_on (problem.cpp:172-255): the manufactured problems 1..3
 // (example 2 has time-dependent coefficients); t_final = 1.

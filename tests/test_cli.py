@@ -38,7 +38,6 @@ def run(cli, *args, cwd=None):
     (["solve", "--example", "1", "--n", "0"], "--n must be in [1, 4096]"),
     (["solve", "--example", "1", "--n", "5000"], "--n must be in [1, 4096]"),
     (["solve", "--example", "1", "--n", "16", "--precond", "ilu"], "unknown preconditioner"),
-    (["solve", "--example", "1", "--n", "16", "--precond", "p2-exact"], "not part of the B200 build"),
     (["solve", "--example", "1", "--n", "16", "--coarse", "direct"], "unknown coarse solve"),
     (["solve", "--example", "1", "--n", "16", "--tol", "-1"], "--tol must be positive"),
     (["solve", "--example", "1", "--n", "16", "--vcycles-per-apply", "17"], "must be in [1, 16]"),
@@ -69,7 +68,8 @@ def read_report(out_dir: Path, command: str):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("example,n,precond", [(1, 32, "mgm"), (2, 32, "mgm"), (3, 16, "p2")])
+@pytest.mark.parametrize("example,n,precond", [(1, 32, "mgm"), (2, 32, "mgm"), (3, 16, "p2"),
+                                               (1, 16, "p2-exact"), (2, 16, "mgm-galerkin")])
 def test_solve_matches_reference(cuda, ref, cli, tmp_path, example, n, precond):
     r = run(cli, "solve", "--example", example, "--n", n, "--precond", precond, "--out-dir", tmp_path)
     assert r.returncode == 0, r.stderr
@@ -79,7 +79,7 @@ def test_solve_matches_reference(cuda, ref, cli, tmp_path, example, n, precond):
     assert (label, n_s, pc) == (str(example), str(n), precond)
     # the reference CLI's defaults: tol 1e-7, restart 20, omega 0.9, m = n (cli.cpp:42-58)
     s = spec(100 + example, n1=n, n2=n, steps=n, tol=1e-7, omega=0.9,
-             precond={"none": 0, "p2": 1, "mgm": 2}[precond])
+             precond={"none": 0, "p2": 1, "mgm": 2, "p2-exact": 3, "mgm-galerkin": 4}[precond])
     ro = ref.time_march(s)
     assert avg == f"{np.mean(ro['its']):.3f}"
     e_ref = ref.error_inf(s, ro["u"], 1.0)

@@ -294,14 +294,14 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   return v;
 }
 
-// all CTAs of the (co-resident) grid reach the barrier; *bar counts arrivals
+// all CTAs of the (co-resident) grid reach the barrier; *bar counts arrivals.
+// The arrival is a release (orders this CTA's partials before it), the
+// polling load an acquire: no full fences on the critical path.
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     while (ld_acquire_u32(bar) < target) __nanosleep(32);
-    __threadfence();
   }
   __syncthreads();
 }
@@ -329,14 +329,12 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     }
     __syncthreads();
     double* const part = partials + (phase & 1) * 2 * gridDim.x;
-    if (threadIdx.x == 0) {
-      double ta = 0.0, tb = 0.0;
-      for (int k = 0; k < kChainThreads / 32; ++k) {
-        ta += red[0][k];
-        tb += red[1][k];
+    if (warp == 0) {  // the 32 warp partials, shuffle tree (fixed order)
+      const double ta = warp_sum(red[0][lane]), tb = warp_sum(red[1][lane]);
+      if (lane == 0) {
+        part[2 * blockIdx.x] = ta;
+        part[2 * blockIdx.x + 1] = tb;
       }
-      part[2 * blockIdx.x] = ta;
-      part[2 * blockIdx.x + 1] = tb;
     }
     ++phase;
     grid_barrier(bar, phase * gridDim.x);

@@ -171,11 +171,22 @@ KrylovWorkspace::KrylovWorkspace(size_t n, size_t restart) : n_(n), rst_(restart
     v_[k].alloc(n);
     ptrs[k] = v_[k].get();
   }
-  for (DevBuf<double>* b : {&t_, &r_, &z_, &w_, &trial_}) b->alloc(n);
+  for (DevBuf<double>* b : {&t_, &r_, &z_, &w_, &w2_, &trial_}) b->alloc(n);
   dsc_.alloc(4 * (rst_ + 2) + 16);
   dcoef_.alloc(rst_ + 1);
   dptr_.upload(ptrs.data(), ptrs.size());
   FDE_CUDA(cudaMallocHost(&hsc_, sizeof(double) * (4 * (rst_ + 2) + 16 + rst_ + 1)));
+  hstride_ = rst_ + 4;
+  FDE_CUDA(cudaMallocHost(&hstep_, sizeof(double) * 2 * hstride_));
+  for (cudaEvent_t& e : ev_step_) FDE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (const char* e = std::getenv("FDE_GMRES_SPECULATE")) speculate_ = e[0] != '0';
+}
+
+KrylovWorkspace::~KrylovWorkspace() {
+  for (cudaEvent_t e : ev_step_)
+    if (e) cudaEventDestroy(e);
+  if (hstep_) cudaFreeHost(hstep_);
+  if (hsc_) cudaFreeHost(hsc_);
 }
 
 void KrylovWorkspace::precondition(const Precond* m, const double* r, double* z,
@@ -273,31 +284,57 @@ KrylovResult KrylovWorkspace::gmres(const StructuredOp& a, const Precond* m,
 
     size_t spanned = 0;
     bool cycle_done = false;
-    for (size_t i = 0; i < rst && !cycle_done; ++i) {
+    // Device work of Arnoldi step i: w = M^-1 A v_i, the Gram-Schmidt
+    // projections, and the staging of the Hessenberg column for the host.
+    // Steps alternate two w buffers and two pinned staging slots so the next
+    // step can be enqueued before the host has read this one.
+    bool enq[2] = {false, false}, chained[2] = {false, false};
+    auto wbuf = [&](size_t i) { return (i & 1) ? w2_.get() : w_.get(); };
+    auto enqueue = [&](size_t i) {
+      double* w = wbuf(i);
       a.apply(v_[i].get(), t_.get(), s);
-      precondition(m, t_.get(), w_.get(), s);
+      precondition(m, t_.get(), w, s);
       // modified Gram-Schmidt (krylov.cpp:92-97): one cooperative launch with
       // w resident in shared memory (and v_{i+1} = w / ||w|| formed on the
       // way out), else each subtraction fused with the next projection: i + 2
       // passes over w instead of 2 (i + 1) + 2
-      const bool chained = red_.mgs_chain(n, w_.get(), dptr_.get(), (int)i, dh, dnorm0, dnrmw,
-                                          v_[i + 1].get(), s);
-      if (!chained) {
-        red_.norm_dot(n, w_.get(), v_[0].get(), dnorm0, dh, s);
+      const bool ch = red_.mgs_chain(n, w, dptr_.get(), (int)i, dh, dnorm0, dnrmw,
+                                     v_[i + 1].get(), s);
+      if (!ch) {
+        red_.norm_dot(n, w, v_[0].get(), dnorm0, dh, s);
         for (size_t k = 0; k <= i; ++k)
-          red_.mgs(n, w_.get(), v_[k].get(), dh + k, k < i ? v_[k + 1].get() : w_.get(),
+          red_.mgs(n, w, v_[k].get(), dh + k, k < i ? v_[k + 1].get() : w,
                    k < i ? dh + k + 1 : dnrmw, k == i, s);
       }
-      fetch(ld + 2, s);
-      for (size_t k = 0; k <= i; ++k) h[i * ld + k] = hsc_[k];
-      const double norm0 = hsc_[ld];
-      double hip = hsc_[ld + 1];
+      copy_small(hstep_ + (i & 1) * hstride_, dsc_.get(), ld + 2, s);
+      FDE_CUDA(cudaEventRecord(ev_step_[i & 1], s));
+      enq[i & 1] = true;
+      chained[i & 1] = ch;
+    };
+    double est_prev = rel0;
+    for (size_t i = 0; i < rst && !cycle_done; ++i) {
+      if (!enq[i & 1]) enqueue(i);
+      // Speculate step i + 1 while the host waits for step i: it only needs
+      // v_{i+1}, which the chained Gram-Schmidt forms on the device.  Worth it
+      // while step i cannot converge (estimates fall by well under 20x per
+      // step here); a step i that converges, breaks down or needs a second
+      // Gram-Schmidt pass discards it.  Arithmetic is unchanged either way.
+      if (speculate_ && chained[i & 1] && i + 1 < rst && est_prev > 20.0 * cfg.tol)
+        enqueue(i + 1);
+      FDE_CUDA(cudaEventSynchronize(ev_step_[i & 1]));
+      const double* hs = hstep_ + (i & 1) * hstride_;
+      enq[i & 1] = false;
+      for (size_t k = 0; k <= i; ++k) h[i * ld + k] = hs[k];
+      const double norm0 = hs[ld];
+      double hip = hs[ld + 1];
       bool reorth = false;
+      double* const w = wbuf(i);
       if (hip < 1e-8 * norm0) {  // second pass (krylov.cpp:98-104)
         reorth = true;
-        red_.dot(n, v_[0].get(), w_.get(), dreo, s);
+        enq[(i + 1) & 1] = false;  // a speculated step used the first-pass v_{i+1}
+        red_.dot(n, v_[0].get(), w, dreo, s);
         for (size_t k = 0; k <= i; ++k)
-          red_.mgs(n, w_.get(), v_[k].get(), dreo + k, k < i ? v_[k + 1].get() : w_.get(),
+          red_.mgs(n, w, v_[k].get(), dreo + k, k < i ? v_[k + 1].get() : w,
                    k < i ? dreo + k + 1 : dnrmw, k == i, s);
         fetch(ld + 2 + i + 1, s);
         for (size_t k = 0; k <= i; ++k) h[i * ld + k] += hsc_[ld + 2 + k];
@@ -320,9 +357,10 @@ KrylovResult KrylovWorkspace::gmres(const StructuredOp& a, const Precond* m,
       ++res.total_iterations;
       spanned = i + 1;
       const double est = std::fabs(g[i + 1]) / norm_b;
+      est_prev = est;
       res.residual_history.push_back(est);
       // (the chained Gram-Schmidt already formed v_{i+1} unless a second pass ran)
-      if (!happy && (!chained || reorth)) copy_scale(n, 1.0 / hip, w_.get(), v_[i + 1].get(), s);
+      if (!happy && (!chained[i & 1] || reorth)) copy_scale(n, 1.0 / hip, w, v_[i + 1].get(), s);
 
       if (est <= cfg.tol || happy) {  // verify the estimate (krylov.cpp:132-149)
         y = back_substitute(h, ld, g, spanned);
@@ -340,6 +378,8 @@ KrylovResult KrylovWorkspace::gmres(const StructuredOp& a, const Precond* m,
         }
       }
     }
+    // a step speculated past the end of the cycle is dropped (its outputs
+    // are rewritten before any use)
     if (!res.converged && !cycle_done) {
       y = back_substitute(h, ld, g, spanned);
       lincomb_into(x, x, y);

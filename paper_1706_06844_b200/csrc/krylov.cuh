@@ -77,6 +77,9 @@ struct KrylovOp {
 class KrylovWorkspace {
  public:
   explicit KrylovWorkspace(size_t n, size_t restart);
+  ~KrylovWorkspace();
+  KrylovWorkspace(const KrylovWorkspace&) = delete;
+  KrylovWorkspace& operator=(const KrylovWorkspace&) = delete;
   size_t n() const { return n_; }
   size_t restart() const { return rst_; }
 
@@ -99,11 +102,17 @@ class KrylovWorkspace {
 
   size_t n_, rst_;
   std::vector<DevBuf<double>> v_;
-  DevBuf<double> t_, r_, z_, w_, trial_, p_, s_, rh_, vv_, tt_;
+  DevBuf<double> t_, r_, z_, w_, w2_, trial_, p_, s_, rh_, vv_, tt_;
   DevBuf<double> dsc_;         // device scalar slots
   DevBuf<double> dcoef_;       // lincomb coefficients
   DevBuf<const double*> dptr_; // lincomb basis pointers
   double* hsc_ = nullptr;      // pinned host mirror of dsc_
+  // GMRES step staging: two pinned slots of the Hessenberg column + norms,
+  // each completed by an event (the next step may be enqueued meanwhile)
+  double* hstep_ = nullptr;
+  size_t hstride_ = 0;
+  cudaEvent_t ev_step_[2] = {nullptr, nullptr};
+  bool speculate_ = true;  // FDE_GMRES_SPECULATE=0 disables
   Reducer red_;
 };
 

@@ -54,3 +54,8 @@ print(f"gaps > 5 us: {len(big) // steps}/step, {sum(big) / 1e3 / steps:.3f} ms/s
       f"gaps <= 5 us: {sum(g for g in gaps if 0 < g <= 5.0) / 1e3 / steps:.3f} ms/step")
 small = [b - a for a, b, _ in ks if b - a < 12.0]
 print(f"kernels < 12 us: {len(small) // steps}/step, {sum(small) / 1e3 / steps:.3f} ms/step busy")
+# the largest gaps with their neighbours
+order = sorted(range(len(gaps)), key=lambda i: -gaps[i])[:12]
+for i in sorted(order):
+    nm = lambda s: s.replace("(anonymous namespace)::", "").replace("fde_b200::", "").split("(")[0][-38:]
+    print(f"  gap {gaps[i]:8.1f} us after {nm(ks[i][2]):38s} before {nm(ks[i + 1][2])}")

@@ -260,6 +260,13 @@ def run_own(args):
     ms_per_step = ms / args.steps
     value = world * args.steps / (ms / 1e3)
     del march, srcs
+    if args.steps_only:  # profiling runs: the launch list holds warm-up + timed steps only
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "steps": args.steps,
+                              "ms_per_step": ms_per_step, "gpu_launches": int(launches),
+                              "note": "--steps-only profiling run (no e2e / roofline legs)"}),
+                  flush=True)
+        return 0
     torch.cuda.empty_cache()
 
     # ---- e2e: public step API with pinned host buffers, H2D source + D2H u per step
@@ -422,6 +429,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--steps-only", action="store_true",
+                    help="time the steps only (for launch-list profiling)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "own":
         log("[bench] warmup raised to 3 (timing rules)")

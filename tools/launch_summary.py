@@ -14,7 +14,9 @@ ki, vi, gi, bi = (hdr.index(k) for k in ("Kernel Name", "Metric Value", "Grid Si
 keep = rows[int(len(rows) * (1 - frac)):]
 agg = collections.defaultdict(lambda: [0, 0.0])
 for r in keep:
-    name = re.sub(r"\(.*", "", r[ki]).replace("void ", "").replace("unnamed>::", "")[:48]
+    raw = r[ki].replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+    raw = raw.replace("fde_b200::", "").replace("void ", "")
+    name = re.sub(r"\(.*", "", raw)[:48]
     key = f"{name} g{r[gi]} b{r[bi]}"
     agg[key][0] += 1
     agg[key][1] += float(r[vi].replace(",", ""))

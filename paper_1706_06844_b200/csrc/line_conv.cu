@@ -1255,6 +1255,7 @@ void launch_any(const P& p, cudaStream_t s) {
     case 10: return FDE_PAIRED ? launch_paired<10>(p, s) : launch_fft<10>(p, s);
     case 11: return FDE_PAIRED ? launch_paired<11>(p, s) : launch_fft<11>(p, s);
     case 12: return launch_fft<12>(p, s);
+    case 13: return launch_fft<13>(p, s);  // n <= 8191 (cfg5's largest grid)
     default: throw InvalidArgument("line length beyond the supported FFT sizes");
   }
 }

@@ -117,7 +117,7 @@ ToeplitzDev::ToeplitzDev(std::vector<double> first_col, std::vector<double> firs
   const size_t M = L_ / 2;
   logM_ = 0;
   while ((size_t(1) << logM_) < M) ++logM_;
-  if (logM_ > 12) throw InvalidArgument("line length beyond the supported FFT sizes (n <= 4095)");
+  if (logM_ > 13) throw InvalidArgument("line length beyond the supported FFT sizes (n <= 8191)");
   // circulant column (structured.cpp:21-30), spectrum scaled by 1/(2L)
   std::vector<cld> c(L_, cld(0.0L, 0.0L));
   for (size_t i = 0; i < n_; ++i) c[i] = (long double)col_[i];

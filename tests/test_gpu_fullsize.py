@@ -177,3 +177,51 @@ def test_march_pipelined_host_io(cuda):
     pipe.wait()
     for m in range(steps):
         np.testing.assert_array_equal(outs[m], want[m])
+
+
+def test_cfg5_largest_grid_n8191(cuda, orc):
+    """cfg5's largest grid (n = 8191, 67 M unknowns, 16384-point circulants):
+    the operator apply at 300 sampled points against direct Toeplitz sums
+    built from the oracle's weights and coefficient fields, apply + apply_rhs
+    = 2 inv_r x, and the zero-guess V-cycle's linearity in b."""
+    import torch
+    n = 8191
+    s = spec(5, n1=n, n2=n, steps=1)
+    p = fde.Problem.preset_config(5, steps=1)
+    op = fde.StructuredFdeOperator.assemble(p, n, n, 1, 1)
+    g = orc.grid(s)
+    dp, dm, ep, em = orc.coefficients(s)
+    x = np.random.default_rng(8191).uniform(-1, 1, n * n)
+    y = op.apply(dev(x)).cpu().numpy()
+    # T = Toeplitz(col = -w_{1..n}, row = (-w_1, -w_0, 0, ...)) (structured.cpp:47-55)
+    def colrow(gamma):
+        _, w = orc.weights(gamma, n)
+        col = -w[1:n + 1]
+        row = np.zeros(n)
+        row[0], row[1] = -w[1], -w[0]
+        return col, row
+    (ca, ra), (cb, rb) = colrow(1.7), colrow(1.3)
+    k = np.arange(n)
+    def tline(col, row, i, v):  # (T v)_i and (T^T v)_i
+        t = np.where(i >= k, col[np.abs(i - k)], row[np.abs(k - i)])
+        tt = np.where(k >= i, col[np.abs(k - i)], row[np.abs(i - k)])
+        return t @ v, tt @ v
+    X = x.reshape(n, n)  # [j, i], x fastest
+    for q in np.random.default_rng(1).integers(0, n * n, 300):
+        i, j = int(q % n), int(q // n)
+        ty, tt = tline(ca, ra, i, X[j])
+        qy, qt = tline(cb, rb, j, X[:, i])
+        ref = g["inv_r"] * x[q] + dp[q] * ty + dm[q] * tt + g["s_over_r"] * (ep[q] * qy + em[q] * qt)
+        assert abs(y[q] - ref) <= 1e-12 * np.abs(y).max(), (i, j, y[q], ref)
+    xd = dev(x)
+    ax = op.apply(xd)
+    s2 = ax + op.apply_rhs(xd)
+    assert float(torch.linalg.norm(s2 - 2 * g["inv_r"] * xd) / torch.linalg.norm(ax)) <= 1e-14
+    del ax, s2
+    h = fde.MgHierarchy.build_geometric(p, n, n, 1, 1, 0.7, fde.COARSE_SWEEPS, 3)
+    assert h.dims() == orc.plan(s)[0]
+    b1, b2 = xd, torch.flip(xd, [0])
+    v = h.vcycle(3.0 * b1 - b2)
+    v12 = 3.0 * h.vcycle(b1) - h.vcycle(b2)
+    assert bool(torch.isfinite(v).all())
+    assert float(torch.linalg.norm(v - v12) / torch.linalg.norm(v)) <= 1e-12

@@ -506,6 +506,9 @@ struct PairedShape {
 #ifndef FDE_L2_PREFETCH_PAIRED
 #define FDE_L2_PREFETCH_PAIRED 0  // measured: cfg4 74.7 -> 75.5 steps/s without (cp.async staging covers dp/dm)
 #endif
+#ifndef FDE_EPI_AHEAD
+#define FDE_EPI_AHEAD 1  // measured: cfg4 75.8 -> 75.9 steps/s
+#endif
 #ifndef FDE_PAIRED_MINB
 #define FDE_PAIRED_MINB 4  // CTAs per SM at M = 2048 (128 registers)
 #endif
@@ -746,6 +749,11 @@ struct LineIO<YPass, EPI> {
   __device__ __forceinline__ Ops fetch_rest(int, double s0, double s1, double) const {
     return Ops{s0, s1};
   }
+  struct Glob {};  // no operands beyond the two staged streams
+  __device__ __forceinline__ Glob fetch_glob(int) const { return Glob{}; }
+  __device__ __forceinline__ Ops combine(const Glob&, double s0, double s1, double) const {
+    return Ops{s0, s1};
+  }
   __device__ __forceinline__ Ops fetch(int d) const { return Ops{ep[d], em[d]}; }
   __device__ __forceinline__ void finish(int d, double ty, double tt, const Ops& o) const {
     const double v = c * (o.ep * ty + o.em * tt);
@@ -785,6 +793,20 @@ struct LineIO<XPass, EPI> {
   __device__ __forceinline__ const double* staged(int k, int d) const { return (k ? dm : dp) + d; }
   // the line's own input stays in shared memory for the epilogue (xv)
   static constexpr bool kKeepX = true;
+  // global operands (Q, rhs/b, dinv) of one position, fetched ahead of use
+  struct Glob {
+    double q, e1, e2;
+  };
+  __device__ __forceinline__ Glob fetch_glob(int d) const {
+    Glob g;
+    g.q = q ? q[d] : 0.0;
+    g.e1 = EPI == EPI_STORE ? 0.0 : e1[d];
+    g.e2 = EPI == EPI_JACOBI ? e2[d] : 0.0;
+    return g;
+  }
+  __device__ __forceinline__ Ops combine(const Glob& g, double s0, double s1, double xv) const {
+    return Ops{xv, s0, s1, g.q, g.e1, g.e2};
+  }
   __device__ __forceinline__ Ops fetch_rest(int d, double s0, double s1, double xv) const {
     Ops o;
     o.x = xv;
@@ -1010,12 +1032,33 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM>()>::THREADS
     //    (2 tl < n) and only the stores predicated: the global loads of a
     //    group are all in flight together (a tail group fetched element by
     //    element behind its own stores serialised one L2 latency per load).
+#if FDE_EPI_AHEAD
+    // group 0's global operands are in flight while the staged streams land
+    typename IO::Glob gn[8];
+    auto fetch_group = [&](int g) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
+        gn[2 * c] = io.fetch_glob(i0 < n ? d : 0);
+        gn[2 * c + 1] = io.fetch_glob(i0 + 1 < n ? d + 1 : 0);
+      }
+    };
+    fetch_group(0);
+#endif
     cp_async_wait_all();
 #pragma unroll
     for (int g = 0; g < H; g += 4) {
       double2 ty[4];
       tmem_ld4(tqy + 4 * g, ty);
       typename IO::Ops o[8];
+#if FDE_EPI_AHEAD
+      // later groups fetch at their top (fetching group g + 4 before group g
+      // is used spills ~230 B in the Jacobi instance: measured 2 % slower)
+      if (g > 0) fetch_group(g);
+      typename IO::Glob gc[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) gc[c] = gn[c];
+#endif
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
@@ -1026,6 +1069,9 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM>()>::THREADS
 #ifdef FDE_EXP_NOEPI
         o[2 * c] = typename IO::Ops{a.x, b.x};
         o[2 * c + 1] = typename IO::Ops{a.y, b.y};
+#elif FDE_EPI_AHEAD
+        o[2 * c] = io.combine(gc[2 * c], a.x, b.x, xv.x);
+        o[2 * c + 1] = io.combine(gc[2 * c + 1], a.y, b.y, xv.y);
 #else
         o[2 * c] = io.fetch_rest(i0 < n ? d : 0, a.x, b.x, xv.x);
         o[2 * c + 1] = io.fetch_rest(i0 + 1 < n ? d + 1 : 0, a.y, b.y, xv.y);

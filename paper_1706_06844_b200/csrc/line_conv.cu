@@ -509,6 +509,9 @@ struct PairedShape {
 #ifndef FDE_EPI_AHEAD
 #define FDE_EPI_AHEAD 1  // measured: cfg4 75.8 -> 75.9 steps/s
 #endif
+#ifndef FDE_X_TMEM
+#define FDE_X_TMEM 1  // measured: n=2047 apply 166.8 -> 165.6 us (L2 flushed), cfg4 +0.1 %
+#endif
 #ifndef FDE_PAIRED_MINB
 #define FDE_PAIRED_MINB 4  // CTAs per SM at M = 2048 (128 registers)
 #endif
@@ -913,6 +916,8 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM>()>::THREADS
   if constexpr (S::NBUF != 1) __syncthreads();
   const uint32_t tq = tbase + ((uint32_t)(warp * 32) << 16);  // this warp's lane quadrant
   const uint32_t tqy = tq, tqt = tq + 4 * P;                    // Qy, Qt column ranges
+  constexpr bool kStashX = IO::kKeepX && FDE_X_TMEM;
+  const uint32_t tqx = tqy + 4 * H;  // stashed row input (Qy columns past T x's)
   const double* const ep0 = smem;            // staged epilogue operands (exchange buffer)
   const double* const ep1 = smem + S::BUF;
 
@@ -994,6 +999,23 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM>()>::THREADS
 #pragma unroll
         for (int c = 0; c < 4; ++c) v[g + c] = t[c];
       }
+      if constexpr (kStashX) {
+        // row pass: the line's own input moves from xbuf to the Qy columns
+        // the first inverse no longer needs (H slots from column 4H), so the
+        // next line's copy overlaps both inverses instead of waiting for the
+        // epilogue (each thread touches only its own xbuf slots)
+        if (it == 0) {
+#pragma unroll
+          for (int g = 0; g < H; g += 4) {
+            double2 t[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              t[c] = *reinterpret_cast<const double2*>(xbuf + 2 * (tl + (g + c) * T));
+            tmem_st4(tqx + 4 * g, t);
+          }
+          if (next < nl) prefetch_x(line_of(next));
+        }
+      }
       cur = 0;
       auto stage_epilogue = [&]() {
         if (it == 0) return;
@@ -1048,8 +1070,9 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM>()>::THREADS
     cp_async_wait_all();
 #pragma unroll
     for (int g = 0; g < H; g += 4) {
-      double2 ty[4];
+      double2 ty[4], tx[4];
       tmem_ld4(tqy + 4 * g, ty);
+      if constexpr (kStashX) tmem_ld4(tqx + 4 * g, tx);
       typename IO::Ops o[8];
 #if FDE_EPI_AHEAD
       // later groups fetch at their top (fetching group g + 4 before group g
@@ -1064,8 +1087,9 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM>()>::THREADS
         const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
         const double2 a = *reinterpret_cast<const double2*>(ep0 + i0);
         const double2 b = *reinterpret_cast<const double2*>(ep1 + i0);
-        const double2 xv = IO::kKeepX ? *reinterpret_cast<const double2*>(xbuf + i0)
-                                      : make_double2(0.0, 0.0);
+        const double2 xv = kStashX       ? tx[c]
+                           : IO::kKeepX ? *reinterpret_cast<const double2*>(xbuf + i0)
+                                        : make_double2(0.0, 0.0);
 #ifdef FDE_EXP_NOEPI
         o[2 * c] = typename IO::Ops{a.x, b.x};
         o[2 * c + 1] = typename IO::Ops{a.y, b.y};
@@ -1084,8 +1108,9 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM>()>::THREADS
         if (live && i0 + 1 < n) io.finish(d + 1, ty[c].y, v[g + c].y, o[2 * c + 1]);
       }
     }
-    // row pass: the next line's input lands once this line's epilogue is done
-    if (IO::kKeepX && next < nl) prefetch_x(line_of(next));
+    // row pass without the stash: the next line's input lands once this
+    // line's epilogue is done
+    if (IO::kKeepX && !kStashX && next < nl) prefetch_x(line_of(next));
   }
   tmem_fence_before();
   __syncthreads();

@@ -512,6 +512,9 @@ struct PairedShape {
 #ifndef FDE_X_TMEM
 #define FDE_X_TMEM 1  // measured: n=2047 apply 166.8 -> 165.6 us (L2 flushed), cfg4 +0.1 %
 #endif
+#ifndef FDE_P8_Y10
+#define FDE_P8_Y10 0  // column passes at M = 1024 with 8 points/thread (one line per CTA): measured no change
+#endif
 #ifndef FDE_PAIRED_MINB
 #define FDE_PAIRED_MINB 4  // CTAs per SM at M = 2048 (128 registers)
 #endif
@@ -855,18 +858,22 @@ struct LineIO<XPass, EPI> {
 #define FDE_PAIRED8 0  // M = 256, 8 points/thread, 4 lines per CTA: measured slower (V-cycle +5 %)
 #endif
 template <int LOGM>
-constexpr int paired_pts() { return LOGM == 8 || (LOGM == 10 && !FDE_P16_M1024) ? 8 : 16; }
-template <int LOGM>
+constexpr int paired_pts_for(bool ypass) {
+  return LOGM == 8 || (LOGM == 10 && (!FDE_P16_M1024 || (ypass && FDE_P8_Y10))) ? 8 : 16;
+}
+template <int LOGM, class Pol>
+constexpr int paired_pts() { return paired_pts_for<LOGM>(std::is_same<Pol, YPass>::value); }
+template <int LOGM, class Pol>
 constexpr int paired_minb() {
-  return paired_pts<LOGM>() == 16 ? FDE_PAIRED_MINB : FDE_PAIRED_MINB10;
+  return paired_pts<LOGM, Pol>() == 16 ? FDE_PAIRED_MINB : FDE_PAIRED_MINB10;
 }
 
 template <int LOGM, class Pol, int EPI>
-__global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM>()>::THREADS,
-                                  paired_minb<LOGM>())
+__global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::THREADS,
+                                  paired_minb<LOGM, Pol>())
     fft_line_kernel_paired(const Pol p) {
   pdl_enter();
-  constexpr int P = paired_pts<LOGM>();
+  constexpr int P = paired_pts<LOGM, Pol>();
   using S = PairedShape<LOGM, P>;
   using IO = LineIO<Pol, EPI>;
   constexpr int T = S::T, H = P / 2, R0 = S::R0, B0 = S::B0, NS0 = S::NS0;
@@ -1259,7 +1266,7 @@ void launch_fft(const P& p, cudaStream_t s) {
 #endif
 template <int LOGM, class P, int EPI>
 void launch_paired_epi(const P& p, cudaStream_t s) {
-  constexpr int PP = paired_pts<LOGM>();
+  constexpr int PP = paired_pts<LOGM, P>();
   using S = PairedShape<LOGM, PP>;
   static bool configured = false;
   if (!configured) {

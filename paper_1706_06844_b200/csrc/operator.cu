@@ -306,8 +306,13 @@ void StructuredOp::sync_host(cudaStream_t s) {
   host_stale_ = false;
 }
 
+// FFT-path column passes read a transposed copy of the input from this many
+// columns up (fewer columns: strided gathers, one transpose launch saved)
+#ifndef FDE_XT_MIN
+#define FDE_XT_MIN 512  // measured: 128 or 256 (-0.4 to -1 %), 1024 (-0.3 %) slower
+#endif
 bool StructuredOp::maps_input() const {
-  return ay_.dev().logM && n1_ >= 512 && transpose_columns_;
+  return ay_.dev().logM && n1_ >= FDE_XT_MIN && transpose_columns_;
 }
 
 void StructuredOp::run(const double* x, double* out, double sign, int epi, const EpiArgs& e,

@@ -496,11 +496,17 @@ struct PairedShape {
   static constexpr size_t LINE_DOUBLES = (size_t(NBUF) * 2 + 1) * BUF;
   static constexpr size_t SMEM = LPC * LINE_DOUBLES * sizeof(double);
   static constexpr int TCOLS = 8 * P;    // Qy (4P words) + Qt (4P words) per thread
+  // TMEM has 128 lanes: a CTA of several 128-thread warpgroups (one long
+  // line, M = 8192) gives each warpgroup its own TCOLS-column range
+  static constexpr int WG = THREADS / 128;
+  static constexpr int TCOLS_CTA = TCOLS * WG;
   static_assert(REM != 0, "paired kernel needs a short stage");
   static constexpr int KX = LP;                 // radix-P -> radix-P exchanges
   static constexpr int KPF = 0;                 // into the paired forward stage
   static constexpr int KPI = P == 16 ? 3 : 2;   // out of the paired inverse stage
-  static_assert(T % 32 == 0 && THREADS == 128, "one lane quadrant per warp");
+  static_assert(T % 32 == 0 && THREADS % 128 == 0 && (LPC == 1 || THREADS == 128),
+                "whole warpgroups, one lane quadrant per warp");
+  static_assert(TCOLS_CTA <= 512 && (TCOLS_CTA & (TCOLS_CTA - 1)) == 0, "TMEM allocation");
 };
 
 #ifndef FDE_L2_PREFETCH_PAIRED
@@ -514,6 +520,9 @@ struct PairedShape {
 #endif
 #ifndef FDE_P8_Y10
 #define FDE_P8_Y10 0  // column passes at M = 1024 with 8 points/thread (one line per CTA): measured no change
+#endif
+#ifndef FDE_PAIRED13
+#define FDE_PAIRED13 1
 #endif
 #ifndef FDE_PAIRED_MINB
 #define FDE_PAIRED_MINB 4  // CTAs per SM at M = 2048 (128 registers)
@@ -864,8 +873,10 @@ constexpr int paired_pts_for(bool ypass) {
 template <int LOGM, class Pol>
 constexpr int paired_pts() { return paired_pts_for<LOGM>(std::is_same<Pol, YPass>::value); }
 template <int LOGM, class Pol>
-constexpr int paired_minb() {
-  return paired_pts<LOGM, Pol>() == 16 ? FDE_PAIRED_MINB : FDE_PAIRED_MINB10;
+constexpr int paired_minb() {  // CTAs per SM; per 128 threads for larger CTAs
+  constexpr int th = PairedShape<LOGM, paired_pts<LOGM, Pol>()>::THREADS;
+  constexpr int b = paired_pts<LOGM, Pol>() == 16 ? FDE_PAIRED_MINB : FDE_PAIRED_MINB10;
+  return b * 128 / th > 0 ? b * 128 / th : 1;
 }
 
 template <int LOGM, class Pol, int EPI>
@@ -914,14 +925,15 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::TH
     for (int k = 0; k < slot; ++k) __nanosleep(FDE_EXP_STAGGER);
   }
 #endif
-  if (warp == 0) tmem_alloc<S::TCOLS>(s_tbase);
+  if (warp == 0) tmem_alloc<S::TCOLS_CTA>(s_tbase);
   if (blockIdx.x * LPC < nl) prefetch_x(line_of(blockIdx.x * LPC));
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   const uint32_t tbase = *s_tbase;  // the first exchange write follows a barrier
   if constexpr (S::NBUF != 1) __syncthreads();
-  const uint32_t tq = tbase + ((uint32_t)(warp * 32) << 16);  // this warp's lane quadrant
+  // this warp's lane quadrant, and its warpgroup's column range
+  const uint32_t tq = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * S::TCOLS);
   const uint32_t tqy = tq, tqt = tq + 4 * P;                    // Qy, Qt column ranges
   constexpr bool kStashX = IO::kKeepX && FDE_X_TMEM;
   const uint32_t tqx = tqy + 4 * H;  // stashed row input (Qy columns past T x's)
@@ -1121,7 +1133,7 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::TH
   }
   tmem_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<S::TCOLS>(tbase);
+  if (warp == 0) tmem_dealloc<S::TCOLS_CTA>(tbase);
 }
 
 // Warp-per-line direct Toeplitz product for short lines (n <= kDirectMax):
@@ -1293,7 +1305,7 @@ void launch_paired_epi(const P& p, cudaStream_t s) {
     const int regs_cta = ((fa.numRegs * 32 + 255) / 256 * 256) * (S::THREADS / 32);
     int per_sm = regs_sm / regs_cta;
     const int by_smem = smem_sm / (int)(S::SMEM + fa.sharedSizeBytes + smem_rsv);
-    const int by_tmem = 512 / S::TCOLS;
+    const int by_tmem = 512 / S::TCOLS_CTA;
     per_sm = per_sm < by_smem ? per_sm : by_smem;
     per_sm = per_sm < by_tmem ? per_sm : by_tmem;
     max_ctas = sms * (per_sm > 0 ? per_sm : 1);
@@ -1339,7 +1351,8 @@ void launch_any(const P& p, cudaStream_t s) {
     case 10: return FDE_PAIRED ? launch_paired<10>(p, s) : launch_fft<10>(p, s);
     case 11: return FDE_PAIRED ? launch_paired<11>(p, s) : launch_fft<11>(p, s);
     case 12: return launch_fft<12>(p, s);
-    case 13: return launch_fft<13>(p, s);  // n <= 8191 (cfg5's largest grid)
+    case 13:  // n <= 8191 (cfg5's largest grid): one 512-thread line per SM
+      return FDE_PAIRED13 ? launch_paired<13>(p, s) : launch_fft<13>(p, s);
     default: throw InvalidArgument("line length beyond the supported FFT sizes");
   }
 }

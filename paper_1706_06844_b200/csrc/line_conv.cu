@@ -482,8 +482,17 @@ __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
 template <int LOGM, int P>
 struct PairedShape {
   static constexpr int M = 1 << LOGM, T = M / P, LP = Log2<P>::v;
-  static constexpr int REM = LOGM % LP;  // log2 R0
+  // log2 M a multiple of log2 P (M = 4096): the last radix-P stage splits
+  // into a radix-P/2 stage and the paired radix-2 stage (16 16 8 | 2)
+  static constexpr bool SPLIT = LOGM % LP == 0;
+  static constexpr int REM = SPLIT ? 1 : LOGM % LP;  // log2 R0
   static constexpr int R0 = 1 << REM;
+  // radix of the stage at NSL, forward (the split stage ends where R0 begins)
+  // and inverse (the split stage follows the paired stage)
+  template <int NSL>
+  static constexpr int fwd_radix() { return SPLIT && LOGM - NSL == LP ? P / 2 : P; }
+  template <int NSL>
+  static constexpr int inv_radix() { return SPLIT && NSL == REM ? P / 2 : P; }
   static constexpr int B0 = P / R0;      // butterflies per thread in the R0 stage
   static constexpr int NS0 = M / R0;     // = B0 * T
   static constexpr int LPC = T >= 128 ? 1 : 128 / T;  // lines per CTA (lockstep)
@@ -500,7 +509,7 @@ struct PairedShape {
   // line, M = 8192) gives each warpgroup its own TCOLS-column range
   static constexpr int WG = THREADS / 128;
   static constexpr int TCOLS_CTA = TCOLS * WG;
-  static_assert(REM != 0, "paired kernel needs a short stage");
+  static_assert(REM != 0 && LOGM >= 2 * LP, "paired kernel needs a short stage");
   static constexpr int KX = LP;                 // radix-P -> radix-P exchanges
   static constexpr int KPF = 0;                 // into the paired forward stage
   static constexpr int KPI = P == 16 ? 3 : 2;   // out of the paired inverse stage
@@ -520,6 +529,9 @@ struct PairedShape {
 #endif
 #ifndef FDE_P8_Y10
 #define FDE_P8_Y10 0  // column passes at M = 1024 with 8 points/thread (one line per CTA): measured no change
+#endif
+#ifndef FDE_PAIRED12
+#define FDE_PAIRED12 1
 #endif
 #ifndef FDE_PAIRED13
 #define FDE_PAIRED13 1
@@ -643,15 +655,15 @@ struct PFwd {
   __device__ __forceinline__ static void run(double2 (&v)[P], double* buf, int& cur, int tl,
                                              const double2* twM, double2 (&w1s)[P]) {
     using S = PairedShape<LOGM, P>;
-    constexpr int LP = S::LP;
-    static_assert(LOGM - NSL >= LP, "");
-    pstage_compute<LOGM, P, false, NSL, P, false, HALF>(v, tl, w1s);
+    constexpr int R = S::template fwd_radix<NSL>();  // P, or P/2 for the split stage
+    static_assert(LOGM - NSL >= Log2<R>::v, "");
+    pstage_compute<LOGM, P, false, NSL, R, false, HALF>(v, tl, w1s);
     double* re = buf + cur * 2 * S::BUF;
     if constexpr (S::NBUF == 1) __syncthreads();
-    constexpr int NX = NSL + LP;
-    constexpr bool LASTP = (LOGM - NX) < LP;  // next stage is the paired R0 stage
+    constexpr int NX = NSL + Log2<R>::v;
+    constexpr bool LASTP = (LOGM - NX) == S::REM;  // next stage is the paired R0 stage
     constexpr int K = LASTP ? S::KPF : S::KX;
-    pstage_write<LOGM, P, NSL, P, false, K>(v, re, re + S::BUF, tl);
+    pstage_write<LOGM, P, NSL, R, false, K>(v, re, re + S::BUF, tl);
     if constexpr (LASTP) {
       pstage_twiddles<LOGM, P, NX, S::R0, true>(w1s, tl, twM);
       __syncthreads();
@@ -659,16 +671,18 @@ struct PFwd {
       cur ^= S::NBUF - 1;
       pstage_compute<LOGM, P, false, NX, S::R0, true, false>(v, tl, w1s);
     } else {
-      pstage_twiddles<LOGM, P, NX, P, false>(w1s, tl, twM);
+      constexpr int RN = S::template fwd_radix<NX>();
+      pstage_twiddles<LOGM, P, NX, RN, false>(w1s, tl, twM);
       __syncthreads();
-      pstage_read<LOGM, P, P, false, K>(v, re, re + S::BUF, tl);
+      pstage_read<LOGM, P, RN, false, K>(v, re, re + S::BUF, tl);
       cur ^= S::NBUF - 1;
       PFwd<LOGM, P, NX, false>::run(v, buf, cur, tl, twM, w1s);
     }
   }
 };
 
-// Inverse radix-P stages from NSL (inputs in v); the last stays in registers.
+// Inverse stages from NSL (radix P, or P/2 for the split stage right after
+// the paired one; inputs in v); the last stays in registers.
 // hook(): called once the last stage's inputs are in registers (the exchange
 // buffer is then free for the epilogue operands, see fft_line_kernel_paired)
 template <int LOGM, int P, int NSL>
@@ -678,39 +692,43 @@ struct PInvTail {
                                              const double2* twM, double2 (&w1s)[P],
                                              const Hook& hook) {
     using S = PairedShape<LOGM, P>;
-    constexpr int LP = S::LP;
-    // last stage: slots q + r B with r >= P/2 hold positions >= M/2 (unused)
-    pstage_compute<LOGM, P, true, NSL, P, false, false, (NSL + LP >= LOGM) && FDE_PRUNE_LAST>(
-        v, tl, w1s);
-    if constexpr (NSL + LP < LOGM) {
+    constexpr int R = S::template inv_radix<NSL>();
+    constexpr int NX = NSL + Log2<R>::v;
+    static_assert(NX <= LOGM, "");
+    // last stage (radix P): slots q + r B with r >= P/2 hold positions >= M/2 (unused)
+    pstage_compute<LOGM, P, true, NSL, R, false, false, (NX >= LOGM) && FDE_PRUNE_LAST>(v, tl,
+                                                                                        w1s);
+    if constexpr (NX < LOGM) {
+      constexpr int RN = S::template inv_radix<NX>();
       double* re = buf + cur * 2 * S::BUF;
       if constexpr (S::NBUF == 1) __syncthreads();
-      pstage_write<LOGM, P, NSL, P, false, S::KX>(v, re, re + S::BUF, tl);
-      pstage_twiddles<LOGM, P, NSL + LP, P, false>(w1s, tl, twM);
+      pstage_write<LOGM, P, NSL, R, false, S::KX>(v, re, re + S::BUF, tl);
+      pstage_twiddles<LOGM, P, NX, RN, false>(w1s, tl, twM);
       __syncthreads();
-      pstage_read<LOGM, P, P, false, S::KX>(v, re, re + S::BUF, tl);
+      pstage_read<LOGM, P, RN, false, S::KX>(v, re, re + S::BUF, tl);
       cur ^= S::NBUF - 1;
-      if constexpr (NSL + 2 * LP >= LOGM) hook();
-      PInvTail<LOGM, P, NSL + LP>::run(v, buf, cur, tl, twM, w1s, hook);
+      if constexpr (NX + Log2<RN>::v >= LOGM) hook();  // the next stage is the last
+      PInvTail<LOGM, P, NX>::run(v, buf, cur, tl, twM, w1s, hook);
     }
   }
 };
 
-// Full inverse: paired R0 stage (NS = 1) on the spectral slots, then radix P.
+// Full inverse: paired R0 stage (NS = 1) on the spectral slots, then the tail.
 template <int LOGM, int P, class Hook>
 __device__ __forceinline__ void pinverse(double2 (&v)[P], double* buf, int& cur, int tl,
                                          const double2* twM, double2 (&w1s)[P],
                                          const Hook& hook) {
   using S = PairedShape<LOGM, P>;
+  constexpr int RN = S::template inv_radix<S::REM>();
   pstage_compute<LOGM, P, true, 0, S::R0, true, false>(v, tl, w1s);
   double* re = buf + cur * 2 * S::BUF;
   if constexpr (S::NBUF == 1) __syncthreads();
   pstage_write<LOGM, P, 0, S::R0, true, S::KPI>(v, re, re + S::BUF, tl);
-  pstage_twiddles<LOGM, P, S::REM, P, false>(w1s, tl, twM);
+  pstage_twiddles<LOGM, P, S::REM, RN, false>(w1s, tl, twM);
   __syncthreads();
-  pstage_read<LOGM, P, P, false, S::KPI>(v, re, re + S::BUF, tl);
+  pstage_read<LOGM, P, RN, false, S::KPI>(v, re, re + S::BUF, tl);
   cur ^= S::NBUF - 1;
-  if constexpr (S::REM + S::LP >= LOGM) hook();
+  if constexpr (S::REM + Log2<RN>::v >= LOGM) hook();  // the tail is one stage
   PInvTail<LOGM, P, S::REM>::run(v, buf, cur, tl, twM, w1s, hook);
 }
 
@@ -1350,7 +1368,7 @@ void launch_any(const P& p, cudaStream_t s) {
     case 9: return FDE_PAIRED9 ? launch_paired<9>(p, s) : launch_fft<9>(p, s);
     case 10: return FDE_PAIRED ? launch_paired<10>(p, s) : launch_fft<10>(p, s);
     case 11: return FDE_PAIRED ? launch_paired<11>(p, s) : launch_fft<11>(p, s);
-    case 12: return launch_fft<12>(p, s);
+    case 12: return FDE_PAIRED12 ? launch_paired<12>(p, s) : launch_fft<12>(p, s);
     case 13:  // n <= 8191 (cfg5's largest grid): one 512-thread line per SM
       return FDE_PAIRED13 ? launch_paired<13>(p, s) : launch_fft<13>(p, s);
     default: throw InvalidArgument("line length beyond the supported FFT sizes");

@@ -1121,7 +1121,8 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::TH
 #endif
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
+        const int i0 = 2 * (tl + (g + c) * T);
+        [[maybe_unused]] const int d = 2 * (g + c) * T;
         const double2 a = *reinterpret_cast<const double2*>(ep0 + i0);
         const double2 b = *reinterpret_cast<const double2*>(ep1 + i0);
         const double2 xv = kStashX       ? tx[c]

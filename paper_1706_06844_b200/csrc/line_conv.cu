@@ -22,6 +22,13 @@ namespace {
 template <int SH>
 __device__ __forceinline__ int swz(int p) { return p ^ ((p >> SH) & 15); }
 
+// spectral constants a_k, b_k of one k: a single 256-bit read-only load
+__device__ __forceinline__ void ld_ab(const double4* p, double2& a, double2& b) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+      : "l"(p));
+}
+
 // ---- small DFTs on registers; INV = false uses exp(-2 pi i / R) -----------
 template <bool INV>
 __device__ __forceinline__ double2 rot90(double2 a) {  // * (-i) forward, * (+i) inverse
@@ -413,8 +420,8 @@ __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
     const int qm = swz<SH>((M - k) & (M - 1));
     const double zr = v[s].x, zi = v[s].y;
     const double mr = ra[qm], mi = ia[qm];
-    const double2* abk = reinterpret_cast<const double2*>(p.blk.ab) + k;
-    const double2 ca = __ldg(abk), cb = __ldg(abk + M);  // a_k, b_k
+    double2 ca, cb;  // a_k, b_k
+    ld_ab(p.blk.ab + k, ca, cb);
     const double t1 = ca.x * zr, t2 = ca.y * zi, t3 = ca.x * zi, t4 = ca.y * zr;
     const double u1 = cb.x * mr, u2 = cb.y * mi, u3 = cb.y * mr, u4 = cb.x * mi;
     v[s] = make_double2((t1 - t2) + (u1 + u2), (t3 + t4) + (u3 - u4));
@@ -991,7 +998,7 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::TH
     //    results go to tensor memory in groups of 4 slots
     {
       const bool t0 = tl == 0;
-      const double2* abv = reinterpret_cast<const double2*>(p.blk.ab);
+      const double4* abv = p.blk.ab;
 #pragma unroll
       for (int g = 0; g < P; g += 4) {
         double2 qy[4], qt[4];
@@ -1006,7 +1013,8 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::TH
 #ifdef FDE_EXP_NOAB
           const double2 ca = make_double2(1.0 + k, 0.5), cb = make_double2(0.25, 0.125 * k);
 #else
-          const double2 ca = __ldg(abv + k), cb = __ldg(abv + S::M + k);
+          double2 ca, cb;
+          ld_ab(abv + k, ca, cb);
 #endif
           const double t1 = ca.x * z.x, t2 = ca.y * z.y, t3 = ca.x * z.y, t4 = ca.y * z.x;
           const double u1 = cb.x * mr, u2 = cb.y * mi, u3 = cb.y * mr, u4 = cb.x * mi;

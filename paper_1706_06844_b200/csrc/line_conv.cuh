@@ -35,7 +35,7 @@ constexpr int kDirectMax = 32;  // n <= this: direct Toeplitz product
 struct LineBlockDev {
   int n;                 // line length
   int logM;              // FFT path: M = 2^logM = L/2; 0 -> direct path
-  const double4* ab;     // spectral constants: a_k at double2 index k, b_k at M + k (operator.cu)
+  const double4* ab;     // spectral constants: (a_k, b_k) at index k, k < M (operator.cu)
   const double2* twM;    // exp(-2 pi i k / M), k < M
   const double* col;     // first column, n entries (direct path)
   const double* row;     // first row, n entries (direct path)

@@ -135,12 +135,8 @@ ToeplitzDev::ToeplitzDev(std::vector<double> first_col, std::vector<double> firs
     const long double cw = cosl(ang), sw = -sinl(ang);
     const cld ak = 2.0L * (a + b + sw * (a - b));
     const cld bk = 2.0L * cld(0.0L, cw) * (a - b);
-    // SoA: a_k at [2k], b_k at [2M + 2k] (one 16-byte stream each)
-    double* abd = reinterpret_cast<double*>(ab.data());
-    abd[2 * k] = (double)ak.real();
-    abd[2 * k + 1] = (double)ak.imag();
-    abd[2 * M + 2 * k] = (double)bk.real();
-    abd[2 * M + 2 * k + 1] = (double)bk.imag();
+    // (a_k, b_k) interleaved: one 32-byte load per k in the line kernels
+    ab[k] = double4{(double)ak.real(), (double)ak.imag(), (double)bk.real(), (double)bk.imag()};
   }
   spec_ = std::make_shared<DevBuf<double4>>();
   spec_->upload(ab.data(), ab.size());

@@ -537,6 +537,9 @@ struct PairedShape {
 #ifndef FDE_P8_Y10
 #define FDE_P8_Y10 0  // column passes at M = 1024 with 8 points/thread (one line per CTA): measured no change
 #endif
+#ifndef FDE_TMEM_LD64
+#define FDE_TMEM_LD64 1  // one 32x32b.x64 load + wait per spectrum (measured +0.1 %)
+#endif
 #ifndef FDE_PAIRED12
 #define FDE_PAIRED12 1
 #endif
@@ -1037,12 +1040,16 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::TH
 #pragma unroll 1
     for (int it = 0; it < n_inv; ++it) {
       const uint32_t src = it ? tqt : tqy;
+      if constexpr (P == 16 && FDE_TMEM_LD64) {
+        tmem_ld16(src, v);  // the whole spectrum in one load and one wait
+      } else {
 #pragma unroll
-      for (int g = 0; g < P; g += 4) {
-        double2 t[4];
-        tmem_ld4(src + 4 * g, t);
+        for (int g = 0; g < P; g += 4) {
+          double2 t[4];
+          tmem_ld4(src + 4 * g, t);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) v[g + c] = t[c];
+          for (int c = 0; c < 4; ++c) v[g + c] = t[c];
+        }
       }
       if constexpr (kStashX) {
         // row pass: the line's own input moves from xbuf to the Qy columns

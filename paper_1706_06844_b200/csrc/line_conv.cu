@@ -531,6 +531,9 @@ struct PairedShape {
 #ifndef FDE_EPI_AHEAD
 #define FDE_EPI_AHEAD 1  // measured: cfg4 75.8 -> 75.9 steps/s
 #endif
+#ifndef FDE_X_TMEM_JACOBI
+#define FDE_X_TMEM_JACOBI 0  // the Jacobi instance spills with the stash: measured +0.4 % steps/s without
+#endif
 #ifndef FDE_X_TMEM
 #define FDE_X_TMEM 1  // measured: n=2047 apply 166.8 -> 165.6 us (L2 flushed), cfg4 +0.1 %
 #endif
@@ -963,7 +966,7 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::TH
   // this warp's lane quadrant, and its warpgroup's column range
   const uint32_t tq = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * S::TCOLS);
   const uint32_t tqy = tq, tqt = tq + 4 * P;                    // Qy, Qt column ranges
-  constexpr bool kStashX = IO::kKeepX && FDE_X_TMEM;
+  constexpr bool kStashX = IO::kKeepX && FDE_X_TMEM && (FDE_X_TMEM_JACOBI || EPI != EPI_JACOBI);
   const uint32_t tqx = tqy + 4 * H;  // stashed row input (Qy columns past T x's)
   const double* const ep0 = smem;            // staged epilogue operands (exchange buffer)
   const double* const ep1 = smem + S::BUF;

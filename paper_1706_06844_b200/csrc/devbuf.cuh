@@ -26,7 +26,9 @@ class DevBuf {
   void alloc(size_t n) {
     release();
     if (n == 0) return;
-    FDE_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+    // 16 bytes of slack: the line kernels' bulk copies move whole 16-byte
+    // chunks and may read up to 8 bytes past the last element of an array
+    FDE_CUDA(cudaMalloc(&p_, n * sizeof(T) + 16));
     n_ = n;
   }
   void upload(const T* h, size_t n) {

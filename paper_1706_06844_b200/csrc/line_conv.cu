@@ -9,6 +9,9 @@
 // free (half-warp phases).  Stage twiddles cost one table load per butterfly;
 // the other powers come from a depth-4 product tree (the FP64 pipe has the
 // headroom, the L1/shared-memory pipe does not).
+#include <initializer_list>
+#include <map>
+#include <mutex>
 #include <type_traits>
 
 #include "line_conv.cuh"
@@ -22,11 +25,21 @@ namespace {
 template <int SH>
 __device__ __forceinline__ int swz(int p) { return p ^ ((p >> SH) & 15); }
 
-// spectral constants a_k, b_k of one k: a single 256-bit read-only load
-__device__ __forceinline__ void ld_ab(const double4* p, double2& a, double2& b) {
-  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
-      : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
-      : "l"(p));
+// Spectral constants of one k from the compact table (operator.cu): a_k at
+// index k (k < M), b_c at M + c for c <= M/2; b_k = b_k (k <= M/2) or
+// -conj(b_{M-k}).  48 KB per block at M = 2048: together with the stage
+// twiddles it stays resident in the L1 the line kernels leave (64 KB).
+template <int M>
+__device__ __forceinline__ void ld_ab(const double2* ab, int k, double2& a, double2& b) {
+#ifdef FDE_EXP_ABSMALL
+  k &= 255;  // timing experiment: an always-L1-resident slice of the table (wrong results)
+#endif
+  asm("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(a.x), "=d"(a.y) : "l"(ab + k));
+  const bool flip = k > M / 2;
+  const double2* pb = ab + M + (flip ? M - k : k);
+  double br, bi;
+  asm("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(br), "=d"(bi) : "l"(pb));
+  b = make_double2(flip ? -br : br, bi);
 }
 
 // ---- small DFTs on registers; INV = false uses exp(-2 pi i / R) -----------
@@ -242,10 +255,10 @@ __device__ __forceinline__ void powers(double2 w1, double2 (&w)[R]) {
 template <int LOGM, int P, int NSL, int R>
 __device__ __forceinline__ void load_tw(double2 (&pre)[P], int tl, const double2* twM) {
   constexpr int M = 1 << LOGM, T = M / P, NS = 1 << NSL, B = P / R;
-  constexpr int TWSH = LOGM - NSL - Log2<R>::v;
-  if constexpr (NS > 1) {
+  (void)M;
+  if constexpr (NS > 1) {  // compact table: exp(-2 pi i j / (NS R)) at NS R / 2 + j
 #pragma unroll
-    for (int q = 0; q < B; ++q) pre[q] = twM[((tl + q * T) & (NS - 1)) << TWSH];  // plain: stays after the barrier
+    for (int q = 0; q < B; ++q) pre[q] = twM[NS * R / 2 + ((tl + q * T) & (NS - 1))];  // plain: stays after the barrier
   }
 }
 
@@ -421,7 +434,7 @@ __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
     const double zr = v[s].x, zi = v[s].y;
     const double mr = ra[qm], mi = ia[qm];
     double2 ca, cb;  // a_k, b_k
-    ld_ab(p.blk.ab + k, ca, cb);
+    ld_ab<M>(p.blk.ab, k, ca, cb);
     const double t1 = ca.x * zr, t2 = ca.y * zi, t3 = ca.x * zi, t4 = ca.y * zr;
     const double u1 = cb.x * mr, u2 = cb.y * mi, u3 = cb.y * mr, u4 = cb.x * mi;
     v[s] = make_double2((t1 - t2) + (u1 + u2), (t3 + t4) + (u3 - u4));
@@ -483,9 +496,33 @@ __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
 // tensor memory (tmem.cuh), so registers hold one 16-point set per thread and
 // three CTAs share an SM.  Exchange buffers alternate (one barrier per
 // exchange).
-#ifndef FDE_PAIRED_DBUF
-#define FDE_PAIRED_DBUF 0
+#ifndef FDE_BAR_IMM
+#define FDE_BAR_IMM 0
 #endif
+#ifndef FDE_CTA_THREADS
+#define FDE_CTA_THREADS 128  // measured: 128-thread CTAs 140 us per n = 2047 apply, 256: 171, 512: 177
+#endif
+// Barrier over one line group of NT threads inside the 512-thread CTA of the
+// paired kernel (named barrier 1 + group index; barrier 0 is the whole CTA).
+template <int NT>
+__device__ __forceinline__ void group_bar() {
+  if constexpr (NT >= FDE_CTA_THREADS) {
+    __syncthreads();
+  } else {
+#if FDE_BAR_IMM
+    // immediate barrier ids (a register id costs an R2UR per barrier)
+    switch ((int)threadIdx.x / NT) {
+      case 0: asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); break;
+      case 1: asm volatile("bar.sync 2, %0;" ::"n"(NT) : "memory"); break;
+      case 2: asm volatile("bar.sync 3, %0;" ::"n"(NT) : "memory"); break;
+      default: asm volatile("bar.sync 4, %0;" ::"n"(NT) : "memory"); break;
+    }
+#else
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)threadIdx.x / NT), "n"(NT) : "memory");
+#endif
+  }
+}
+
 template <int LOGM, int P>
 struct PairedShape {
   static constexpr int M = 1 << LOGM, T = M / P, LP = Log2<P>::v;
@@ -504,39 +541,37 @@ struct PairedShape {
   static constexpr int NS0 = M / R0;     // = B0 * T
   static constexpr int LPC = T >= 128 ? 1 : 128 / T;  // lines per CTA (lockstep)
   static constexpr int THREADS = T * LPC;
-  static constexpr int BUF = M;          // doubles per re / im plane
+  static constexpr int BUF = M;          // doubles per landing plane (input line / coefficient line)
+  static constexpr int SLOTS = M + (M >> 3);  // padded 16-byte exchange slots (pslot, K >= 3)
   // alternating exchange buffers need an even exchange count per transform
   // (both inverses start on buffer 0 with no barrier in between)
-  static constexpr int NBUF = (FDE_PAIRED_DBUF && (LOGM / LP) % 2 == 0) ? 2 : 1;
-  // per line: exchange buffer(s) + the next line's input (BUF doubles)
-  static constexpr size_t LINE_DOUBLES = (size_t(NBUF) * 2 + 1) * BUF;
-  static constexpr size_t SMEM = LPC * LINE_DOUBLES * sizeof(double);
+  // per line: the exchange buffer (it also stages the line's input and the
+  // epilogue coefficient streams); after the lines a control block with two
+  // mbarriers per line slot and the TMEM base address
+  // per line: the padded exchange slots; their first 2 BUF doubles double as
+  // the two coefficient planes of the epilogue
+  static constexpr size_t LINE_DOUBLES = size_t(2) * SLOTS;
+  // One CTA of 512 threads per SM holds NG independent line groups (each the
+  // THREADS threads of LPC lockstep lines, synchronised by its own named
+  // barrier): 4 x 32 KB of exchange buffers plus one small control block fit
+  // the 132 KB shared-memory configuration, which leaves ~90 KB of L1
+  // (measured, tools/l1_probe.cu) -- separate 128-thread CTAs would each pay
+  // the control block and land in the 164 KB configuration (~56 KB of L1).
+  static constexpr int CTA_THREADS = FDE_CTA_THREADS > THREADS ? FDE_CTA_THREADS : THREADS;
+  static constexpr size_t CTRL_BYTES = 128;
   static constexpr int TCOLS = 8 * P;    // Qy (4P words) + Qt (4P words) per thread
   // TMEM has 128 lanes: a CTA of several 128-thread warpgroups (one long
   // line, M = 8192) gives each warpgroup its own TCOLS-column range
   static constexpr int WG = THREADS / 128;
-  static constexpr int TCOLS_CTA = TCOLS * WG;
+  static constexpr int NG = CTA_THREADS / THREADS;  // line groups per CTA
+  static constexpr int TCOLS_CTA = TCOLS * WG * NG;
+  static constexpr size_t SMEM = size_t(NG) * LPC * LINE_DOUBLES * sizeof(double) + CTRL_BYTES;
   static_assert(REM != 0 && LOGM >= 2 * LP, "paired kernel needs a short stage");
-  static constexpr int KX = LP;                 // radix-P -> radix-P exchanges
-  static constexpr int KPF = 0;                 // into the paired forward stage
-  static constexpr int KPI = P == 16 ? 3 : 2;   // out of the paired inverse stage
   static_assert(T % 32 == 0 && THREADS % 128 == 0 && (LPC == 1 || THREADS == 128),
                 "whole warpgroups, one lane quadrant per warp");
   static_assert(TCOLS_CTA <= 512 && (TCOLS_CTA & (TCOLS_CTA - 1)) == 0, "TMEM allocation");
 };
 
-#ifndef FDE_L2_PREFETCH_PAIRED
-#define FDE_L2_PREFETCH_PAIRED 0  // measured: cfg4 74.7 -> 75.5 steps/s without (cp.async staging covers dp/dm)
-#endif
-#ifndef FDE_EPI_AHEAD
-#define FDE_EPI_AHEAD 1  // measured: cfg4 75.8 -> 75.9 steps/s
-#endif
-#ifndef FDE_X_TMEM_JACOBI
-#define FDE_X_TMEM_JACOBI 0  // the Jacobi instance spills with the stash: measured +0.4 % steps/s without
-#endif
-#ifndef FDE_X_TMEM
-#define FDE_X_TMEM 1  // measured: n=2047 apply 166.8 -> 165.6 us (L2 flushed), cfg4 +0.1 %
-#endif
 #ifndef FDE_P8_Y10
 #define FDE_P8_Y10 0  // column passes at M = 1024 with 8 points/thread (one line per CTA): measured no change
 #endif
@@ -548,12 +583,6 @@ struct PairedShape {
 #endif
 #ifndef FDE_PAIRED13
 #define FDE_PAIRED13 1
-#endif
-#ifndef FDE_PAIRED_MINB
-#define FDE_PAIRED_MINB 4  // CTAs per SM at M = 2048 (128 registers)
-#endif
-#ifndef FDE_PAIRED_MINB10
-#define FDE_PAIRED_MINB10 5
 #endif
 
 // butterfly handled in slot q of the paired R0 stage
@@ -599,29 +628,35 @@ __device__ __forceinline__ void pstage_compute(double2 (&v)[P], int tl, const do
 template <int LOGM, int P, int NSL, int R, bool PAIRED>
 __device__ __forceinline__ void pstage_twiddles(double2 (&w1s)[P], int tl, const double2* twM) {
   constexpr int T = (1 << LOGM) / P, B = P / R, NS = 1 << NSL;
-  constexpr int TWSH = LOGM - NSL - Log2<R>::v;
-  if constexpr (NS > 1) {
+  if constexpr (NS > 1) {  // compact table: exp(-2 pi i j / (NS R)) at NS R / 2 + j
 #pragma unroll
     for (int q = 0; q < B; ++q) {
       const int j = PAIRED ? paired_bfly<B, T>(tl, q) : tl + q * T;
-      w1s[q] = twM[(j & (NS - 1)) << TWSH];
+      w1s[q] = twM[NS * R / 2 + (j & (NS - 1))];
     }
   }
 }
 
-// Stockham write of a finished stage (NSL, R) to plane (re, im)
-// Exchange-buffer swizzle p ^ ((p >> K) & 15) (K = 0: none).  Each exchange
-// picks the K that makes both its write and its read pattern free of 8-byte
-// bank conflicts (the paired stage's (j, NS - j) accesses need their own).
+// Exchange buffer of the paired kernel: one 16-byte slot per complex value,
+// padded: slot(p) = p + (p >> K).  Each exchange picks K from its write
+// pattern (write_pad) so that every 128-bit access of a quarter warp hits
+// eight distinct 16-byte bank groups, on the write and on the read side
+// (tools/bank_sim.py enumerates all of them).  Every butterfly's R accesses
+// are base + compile-time offsets: slot(p0 + r S) - slot(p0) does not depend
+// on the thread (checked by the same tool), so an exchange costs one address
+// per butterfly and no index arithmetic per access -- the XOR swizzle this
+// replaces spent ~2.5 integer instructions per access, a fifth of all issued
+// instructions.
 template <int K>
-__device__ __forceinline__ int swzk(int p) {
-  if constexpr (K == 0) return p;
-  else return p ^ ((p >> K) & 15);
+__host__ __device__ constexpr int pslot(int p) { return K ? p + (p >> K) : p; }
+template <int NSL, int R>
+constexpr int write_pad() {
+  return NSL >= 3 ? 0 : (Log2<R>::v > 3 ? Log2<R>::v : 3);
 }
 
+// Stockham write of a finished stage (NSL, R)
 template <int LOGM, int P, int NSL, int R, bool PAIRED, int K>
-__device__ __forceinline__ void pstage_write(const double2 (&v)[P], double* re, double* im,
-                                             int tl) {
+__device__ __forceinline__ void pstage_write(const double2 (&v)[P], double2* buf, int tl) {
 #ifdef FDE_EXP_NOXCHG
   return;
 #endif
@@ -630,19 +665,15 @@ __device__ __forceinline__ void pstage_write(const double2 (&v)[P], double* re, 
   for (int q = 0; q < B; ++q) {
     const int j = PAIRED ? paired_bfly<B, T>(tl, q) : tl + q * T;
     const int base = ((j >> NSL) << (NSL + Log2<R>::v)) + (j & (NS - 1));
+    double2* const b = buf + pslot<K>(base);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int p = swzk<K>(base + r * NS);
-      re[p] = v[q + r * B].x;
-      im[p] = v[q + r * B].y;
-    }
+    for (int r = 0; r < R; ++r) b[pslot<K>(r * NS)] = v[q + r * B];
   }
 }
 
 // inputs of stage (R, PAIRED): butterfly j reads j + r * M / R
 template <int LOGM, int P, int R, bool PAIRED, int K>
-__device__ __forceinline__ void pstage_read(double2 (&v)[P], const double* re, const double* im,
-                                            int tl) {
+__device__ __forceinline__ void pstage_read(double2 (&v)[P], const double2* buf, int tl) {
 #ifdef FDE_EXP_NOXCHG
   return;
 #endif
@@ -650,11 +681,9 @@ __device__ __forceinline__ void pstage_read(double2 (&v)[P], const double* re, c
 #pragma unroll
   for (int q = 0; q < B; ++q) {
     const int j = PAIRED ? paired_bfly<B, T>(tl, q) : tl + q * T;
+    const double2* const b = buf + pslot<K>(j);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int p = swzk<K>(j + r * (M / R));
-      v[q + r * B] = make_double2(re[p], im[p]);
-    }
+    for (int r = 0; r < R; ++r) v[q + r * B] = b[pslot<K>(r * (M / R))];
   }
 }
 
@@ -662,34 +691,38 @@ __device__ __forceinline__ void pstage_read(double2 (&v)[P], const double* re, c
 #define FDE_PRUNE_LAST 1
 #endif
 // Forward transform, radix-P stages from NSL, ending with the paired R0 stage.
-// On entry the stage at NSL has its inputs in v; the exchange buffer toggles.
+// On entry the stage at NSL has its inputs in v.  One exchange buffer: a
+// barrier before the writes (everyone has read the previous contents) and one
+// before the reads.
 template <int LOGM, int P, int NSL, bool HALF>
 struct PFwd {
-  __device__ __forceinline__ static void run(double2 (&v)[P], double* buf, int& cur, int tl,
-                                             const double2* twM, double2 (&w1s)[P]) {
+  // pre(): called once the paired stage's inputs are in registers (the
+  // spectral step follows that stage's butterflies)
+  template <class Pre>
+  __device__ __forceinline__ static void run(double2 (&v)[P], double2* buf, int tl,
+                                             const double2* twM, double2 (&w1s)[P],
+                                             const Pre& pre) {
     using S = PairedShape<LOGM, P>;
     constexpr int R = S::template fwd_radix<NSL>();  // P, or P/2 for the split stage
     static_assert(LOGM - NSL >= Log2<R>::v, "");
     pstage_compute<LOGM, P, false, NSL, R, false, HALF>(v, tl, w1s);
-    double* re = buf + cur * 2 * S::BUF;
-    if constexpr (S::NBUF == 1) __syncthreads();
+    group_bar<S::THREADS>();
     constexpr int NX = NSL + Log2<R>::v;
     constexpr bool LASTP = (LOGM - NX) == S::REM;  // next stage is the paired R0 stage
-    constexpr int K = LASTP ? S::KPF : S::KX;
-    pstage_write<LOGM, P, NSL, R, false, K>(v, re, re + S::BUF, tl);
+    constexpr int K = write_pad<NSL, R>();
+    pstage_write<LOGM, P, NSL, R, false, K>(v, buf, tl);
     if constexpr (LASTP) {
       pstage_twiddles<LOGM, P, NX, S::R0, true>(w1s, tl, twM);
-      __syncthreads();
-      pstage_read<LOGM, P, S::R0, true, K>(v, re, re + S::BUF, tl);
-      cur ^= S::NBUF - 1;
+      group_bar<S::THREADS>();
+      pstage_read<LOGM, P, S::R0, true, K>(v, buf, tl);
+      pre();
       pstage_compute<LOGM, P, false, NX, S::R0, true, false>(v, tl, w1s);
     } else {
       constexpr int RN = S::template fwd_radix<NX>();
       pstage_twiddles<LOGM, P, NX, RN, false>(w1s, tl, twM);
-      __syncthreads();
-      pstage_read<LOGM, P, RN, false, K>(v, re, re + S::BUF, tl);
-      cur ^= S::NBUF - 1;
-      PFwd<LOGM, P, NX, false>::run(v, buf, cur, tl, twM, w1s);
+      group_bar<S::THREADS>();
+      pstage_read<LOGM, P, RN, false, K>(v, buf, tl);
+      PFwd<LOGM, P, NX, false>::run(v, buf, tl, twM, w1s, pre);
     }
   }
 };
@@ -701,7 +734,7 @@ struct PFwd {
 template <int LOGM, int P, int NSL>
 struct PInvTail {
   template <class Hook>
-  __device__ __forceinline__ static void run(double2 (&v)[P], double* buf, int& cur, int tl,
+  __device__ __forceinline__ static void run(double2 (&v)[P], double2* buf, int tl,
                                              const double2* twM, double2 (&w1s)[P],
                                              const Hook& hook) {
     using S = PairedShape<LOGM, P>;
@@ -713,36 +746,34 @@ struct PInvTail {
                                                                                         w1s);
     if constexpr (NX < LOGM) {
       constexpr int RN = S::template inv_radix<NX>();
-      double* re = buf + cur * 2 * S::BUF;
-      if constexpr (S::NBUF == 1) __syncthreads();
-      pstage_write<LOGM, P, NSL, R, false, S::KX>(v, re, re + S::BUF, tl);
+      constexpr int K = write_pad<NSL, R>();
+      group_bar<S::THREADS>();
+      pstage_write<LOGM, P, NSL, R, false, K>(v, buf, tl);
       pstage_twiddles<LOGM, P, NX, RN, false>(w1s, tl, twM);
-      __syncthreads();
-      pstage_read<LOGM, P, RN, false, S::KX>(v, re, re + S::BUF, tl);
-      cur ^= S::NBUF - 1;
+      group_bar<S::THREADS>();
+      pstage_read<LOGM, P, RN, false, K>(v, buf, tl);
       if constexpr (NX + Log2<RN>::v >= LOGM) hook();  // the next stage is the last
-      PInvTail<LOGM, P, NX>::run(v, buf, cur, tl, twM, w1s, hook);
+      PInvTail<LOGM, P, NX>::run(v, buf, tl, twM, w1s, hook);
     }
   }
 };
 
 // Full inverse: paired R0 stage (NS = 1) on the spectral slots, then the tail.
 template <int LOGM, int P, class Hook>
-__device__ __forceinline__ void pinverse(double2 (&v)[P], double* buf, int& cur, int tl,
+__device__ __forceinline__ void pinverse(double2 (&v)[P], double2* buf, int tl,
                                          const double2* twM, double2 (&w1s)[P],
                                          const Hook& hook) {
   using S = PairedShape<LOGM, P>;
   constexpr int RN = S::template inv_radix<S::REM>();
+  constexpr int K = write_pad<0, S::R0>();
   pstage_compute<LOGM, P, true, 0, S::R0, true, false>(v, tl, w1s);
-  double* re = buf + cur * 2 * S::BUF;
-  if constexpr (S::NBUF == 1) __syncthreads();
-  pstage_write<LOGM, P, 0, S::R0, true, S::KPI>(v, re, re + S::BUF, tl);
+  group_bar<S::THREADS>();
+  pstage_write<LOGM, P, 0, S::R0, true, K>(v, buf, tl);
   pstage_twiddles<LOGM, P, S::REM, RN, false>(w1s, tl, twM);
-  __syncthreads();
-  pstage_read<LOGM, P, RN, false, S::KPI>(v, re, re + S::BUF, tl);
-  cur ^= S::NBUF - 1;
+  group_bar<S::THREADS>();
+  pstage_read<LOGM, P, RN, false, K>(v, buf, tl);
   if constexpr (S::REM + Log2<RN>::v >= LOGM) hook();  // the tail is one stage
-  PInvTail<LOGM, P, S::REM>::run(v, buf, cur, tl, twM, w1s, hook);
+  PInvTail<LOGM, P, S::REM>::run(v, buf, tl, twM, w1s, hook);
 }
 
 // spectral partner slot of slot s = q + r * B0 (tl != 0 / tl == 0)
@@ -755,61 +786,93 @@ constexpr int partner_slot(int s, bool t0) {
   return q2 + r2 * B;
 }
 
-// Per-line I/O views for the paired kernel: pointers are offset to the
-// thread's first position 2*tl once, so every slot's accesses use
-// compile-time displacements d = pos - 2*tl (no per-access 64-bit index math).
+// ---------------------------------------------------------------------------
+// Line I/O of the paired kernel.
+//
+// Every stream of a pass (input line, coefficient lines, Q, b, dinv, output)
+// has the same line offset line * n, and the host checks that all base
+// addresses agree modulo 16 bytes, so one parity sx = (par + line * n) & 1
+// says whether a line starts 8 bytes past a 16-byte boundary.  Such a line is
+// processed as the VIRTUAL line (0, x_0, ..., x_{n-1}) of length nv = n + 1:
+// a Toeplitz product is shift invariant, so output element e sits at virtual
+// position e + sx, and every 16-byte pair (2m, 2m+1) of virtual positions is
+// aligned in all streams -- bulk copies, 128-bit loads and 128-bit stores
+// apply to odd lines too (n + 1 <= M is checked by the host).
+// Pointers below address virtual position 0 (= element -sx).
+__device__ __forceinline__ double2 ld_pair(const double* v0, int pv, int sx, int nv) {
+  const double* a = v0 + pv;
+  if (pv >= sx && pv + 1 < nv) return __ldcg(reinterpret_cast<const double2*>(a));
+  double2 r = make_double2(0.0, 0.0);  // edge pairs: element by element
+  if (pv >= sx && pv < nv) r.x = __ldcg(a);
+  if (pv + 1 < nv) r.y = __ldcg(a + 1);
+  return r;
+}
+__device__ __forceinline__ void st_pair(double* v0, int pv, int sx, int nv, bool live, double2 r) {
+  double* a = v0 + pv;
+  if (!live) return;
+  if (pv >= sx && pv + 1 < nv) {
+    *reinterpret_cast<double2*>(a) = r;
+  } else {
+    if (pv >= sx && pv < nv) a[0] = r.x;
+    if (pv + 1 < nv) a[1] = r.y;
+  }
+}
+
 template <class Pol, int EPI>
 struct LineIO;
 
-// YPass: EPI carries the layout flags, bit 0 = xT (x transposed), bit 1 = qT
+// YPass: EPI bit 1 = qT (Q written transposed, i.e. contiguous along the line).
+// Stream 0 (ep) is staged through plane 0 of the exchange buffer, stream 1
+// (em) is loaded in 16-byte pairs with the group's other global operands
+// (plane 1 receives the next line's input meanwhile).
 template <int EPI>
 struct LineIO<YPass, EPI> {
-  static constexpr bool XT = EPI & 1, QT = (EPI >> 1) & 1;
+  static constexpr bool QT = (EPI >> 1) & 1;
+  static constexpr int G = 4;  // slots per epilogue group
   const double* x;
   const double* ep;
   const double* em;
   double* q;
-  int n1;
+  size_t n1;
   double c;
-  struct Ops {
-    double ep, em;
-  };
-  __device__ __forceinline__ LineIO(const YPass& p, int line, int pos0) {
-    const size_t n1s = p.n1, n2 = p.n2;
-    n1 = p.n1;
-    x = XT ? p.x + line * n2 + pos0 : p.x + line + pos0 * n1s;
-    ep = p.epT + line * n2 + pos0;
-    em = p.emT + line * n2 + pos0;
-    q = QT ? p.q + line * n2 + pos0 : p.q + line + pos0 * n1s;
+  int sx, nv;
+  __device__ __forceinline__ LineIO(const YPass& p, int line, int sx_) {
+    const ptrdiff_t o = (ptrdiff_t)line * p.n2 - sx_;
+    sx = sx_;
+    nv = p.n2 + sx_;
+    n1 = (size_t)p.n1;
+    x = p.x + o;
+    ep = p.epT + o;
+    em = p.emT + o;
+    q = QT ? p.q + o : p.q + line - (ptrdiff_t)sx_ * p.n1;
     c = p.c;
   }
-  __device__ __forceinline__ double load(int d) const {
-    return XT ? x[d] : x[(size_t)d * n1];
-  }
-  __device__ __forceinline__ const double* xaddr(int d) const {
-    return XT ? x + d : x + (size_t)d * n1;
-  }
-  // the two operand streams staged through shared memory, and the rest
-  __device__ __forceinline__ const double* staged(int k, int d) const { return (k ? em : ep) + d; }
-  static constexpr bool kKeepX = false;  // the epilogue does not read x
-  __device__ __forceinline__ Ops fetch_rest(int, double s0, double s1, double) const {
-    return Ops{s0, s1};
-  }
-  struct Glob {};  // no operands beyond the two staged streams
-  __device__ __forceinline__ Glob fetch_glob(int) const { return Glob{}; }
-  __device__ __forceinline__ Ops combine(const Glob&, double s0, double s1, double) const {
-    return Ops{s0, s1};
-  }
-  __device__ __forceinline__ Ops fetch(int d) const { return Ops{ep[d], em[d]}; }
-  __device__ __forceinline__ void finish(int d, double ty, double tt, const Ops& o) const {
-    const double v = c * (o.ep * ty + o.em * tt);
-    if (QT) q[d] = v;
-    else q[(size_t)d * n1] = v;
+  __device__ __forceinline__ const double* input() const { return x; }
+  __device__ __forceinline__ const double* staged(int k) const { return k ? em : ep; }
+  struct Glob {
+    double2 s1;
+  };
+  __device__ __forceinline__ Glob fetch_glob(int pv) const { return Glob{ld_pair(em, pv, sx, nv)}; }
+  __device__ __forceinline__ void prefetch_rest(uint32_t) const {}
+  __device__ __forceinline__ void finish(int pv, bool live, double2 ty, double2 tt, double2 s0,
+                                         const Glob& g) const {
+    const double2 s1 = g.s1;
+    const double2 v = make_double2(c * (s0.x * ty.x + s1.x * tt.x), c * (s0.y * ty.y + s1.y * tt.y));
+    if (QT) {
+      st_pair(q, pv, sx, nv, live, v);
+    } else if (live) {
+      if (pv >= sx && pv < nv) q[(size_t)pv * n1] = v.x;
+      if (pv + 1 < nv) q[(size_t)(pv + 1) * n1] = v.y;
+    }
   }
 };
 
+// XPass: dp is staged through plane 0 of the exchange buffer; dm, the line's
+// own input (again, for inv_r x), Q, b, dinv / src are loaded in 16-byte
+// pairs, a group of slots at a time.
 template <int EPI>
 struct LineIO<XPass, EPI> {
+  static constexpr int G = EPI == EPI_STORE ? 4 : 2;
   const double* x;
   const double* dp;
   const double* dm;
@@ -818,11 +881,11 @@ struct LineIO<XPass, EPI> {
   const double* e2;  // dinv (JACOBI)
   double* out;
   double inv_r, sign, s2;  // s2: src_scale (RHS) or omega (JACOBI)
-  struct Ops {
-    double x, dp, dm, q, e1, e2;
-  };
-  __device__ __forceinline__ LineIO(const XPass& p, int line, int pos0) {
-    const size_t o = (size_t)line * p.n1 + pos0;
+  int sx, nv;
+  __device__ __forceinline__ LineIO(const XPass& p, int line, int sx_) {
+    const ptrdiff_t o = (ptrdiff_t)line * p.n1 - sx_;
+    sx = sx_;
+    nv = p.n1 + sx_;
     x = p.x + o;
     dp = p.dp + o;
     dm = p.dm + o;
@@ -834,55 +897,43 @@ struct LineIO<XPass, EPI> {
     sign = p.sign;
     s2 = EPI == EPI_RHS ? p.src_scale : p.omega;
   }
-  __device__ __forceinline__ double load(int d) const { return x[d]; }
-  __device__ __forceinline__ const double* xaddr(int d) const { return x + d; }
-  __device__ __forceinline__ const double* staged(int k, int d) const { return (k ? dm : dp) + d; }
-  // the line's own input stays in shared memory for the epilogue (xv)
-  static constexpr bool kKeepX = true;
-  // global operands (Q, rhs/b, dinv) of one position, fetched ahead of use
+  __device__ __forceinline__ const double* input() const { return x; }
+  __device__ __forceinline__ const double* staged(int k) const { return k ? dm : dp; }
   struct Glob {
-    double q, e1, e2;
+    double2 s1, x, q, e1, e2;
   };
-  __device__ __forceinline__ Glob fetch_glob(int d) const {
+  __device__ __forceinline__ Glob fetch_glob(int pv) const {
     Glob g;
-    g.q = q ? q[d] : 0.0;
-    g.e1 = EPI == EPI_STORE ? 0.0 : e1[d];
-    g.e2 = EPI == EPI_JACOBI ? e2[d] : 0.0;
+    g.s1 = ld_pair(dm, pv, sx, nv);
+    g.x = ld_pair(x, pv, sx, nv);
+    g.q = q ? ld_pair(q, pv, sx, nv) : make_double2(0.0, 0.0);
+    g.e1 = EPI == EPI_STORE ? make_double2(0.0, 0.0) : ld_pair(e1, pv, sx, nv);
+    g.e2 = EPI == EPI_JACOBI ? ld_pair(e2, pv, sx, nv) : make_double2(0.0, 0.0);
     return g;
   }
-  __device__ __forceinline__ Ops combine(const Glob& g, double s0, double s1, double xv) const {
-    return Ops{xv, s0, s1, g.q, g.e1, g.e2};
+  // warm L2 with the line's directly loaded operands (Q was just written)
+  __device__ __forceinline__ void prefetch_rest(uint32_t bytes) const {
+    if constexpr (EPI != EPI_STORE) bulk_prefetch_l2(e1, bytes);
+    if constexpr (EPI == EPI_JACOBI) bulk_prefetch_l2(e2, bytes);
   }
-  __device__ __forceinline__ Ops fetch_rest(int d, double s0, double s1, double xv) const {
-    Ops o;
-    o.x = xv;
-    o.dp = s0;
-    o.dm = s1;
-    o.q = q ? q[d] : 0.0;
-    o.e1 = EPI == EPI_STORE ? 0.0 : e1[d];
-    o.e2 = EPI == EPI_JACOBI ? e2[d] : 0.0;
-    return o;
-  }
-  __device__ __forceinline__ Ops fetch(int d) const {
-    Ops o;
-    o.x = x[d];
-    o.dp = dp[d];
-    o.dm = dm[d];
-    o.q = q ? q[d] : 0.0;
-    o.e1 = EPI == EPI_STORE ? 0.0 : e1[d];
-    o.e2 = EPI == EPI_JACOBI ? e2[d] : 0.0;
-    return o;
-  }
-  __device__ __forceinline__ void finish(int d, double ty, double tt, const Ops& o) const {
+  __device__ __forceinline__ double one(double xv, double a, double b, double qv, double f1,
+                                        double f2, double ty, double tt) const {
     // structured.cpp:128,134-135,146: y = inv_r x; y += s dp t; y += s dm tt; y += Q
-    double y = inv_r * o.x;
-    y += sign * o.dp * ty;
-    y += sign * o.dm * tt;
-    if (q) y += o.q;
-    if constexpr (EPI == EPI_RHS) out[d] = y + s2 * o.e1;
-    else if constexpr (EPI == EPI_RESID) out[d] = o.e1 - y;
-    else if constexpr (EPI == EPI_JACOBI) out[d] = o.x + s2 * o.e2 * (o.e1 - y);
-    else out[d] = y;
+    double y = inv_r * xv;
+    y += sign * a * ty;
+    y += sign * b * tt;
+    if (q) y += qv;
+    if constexpr (EPI == EPI_RHS) return y + s2 * f1;
+    else if constexpr (EPI == EPI_RESID) return f1 - y;
+    else if constexpr (EPI == EPI_JACOBI) return xv + s2 * f2 * (f1 - y);
+    else return y;
+  }
+  __device__ __forceinline__ void finish(int pv, bool live, double2 ty, double2 tt, double2 s0,
+                                         const Glob& g) const {
+    const double2 s1 = g.s1;
+    const double2 v = make_double2(one(g.x.x, s0.x, s1.x, g.q.x, g.e1.x, g.e2.x, ty.x, tt.x),
+                                   one(g.x.y, s0.y, s1.y, g.q.y, g.e1.y, g.e2.y, ty.y, tt.y));
+    st_pair(out, pv, sx, nv, live, v);
   }
 };
 
@@ -897,22 +948,18 @@ struct LineIO<XPass, EPI> {
 #ifndef FDE_PAIRED8
 #define FDE_PAIRED8 0  // M = 256, 8 points/thread, 4 lines per CTA: measured slower (V-cycle +5 %)
 #endif
+#ifndef FDE_BULK_PF
+#define FDE_BULK_PF 1  // L2 bulk prefetch of the line's operand streams at line start
+#endif
 template <int LOGM>
 constexpr int paired_pts_for(bool ypass) {
   return LOGM == 8 || (LOGM == 10 && (!FDE_P16_M1024 || (ypass && FDE_P8_Y10))) ? 8 : 16;
 }
 template <int LOGM, class Pol>
 constexpr int paired_pts() { return paired_pts_for<LOGM>(std::is_same<Pol, YPass>::value); }
-template <int LOGM, class Pol>
-constexpr int paired_minb() {  // CTAs per SM; per 128 threads for larger CTAs
-  constexpr int th = PairedShape<LOGM, paired_pts<LOGM, Pol>()>::THREADS;
-  constexpr int b = paired_pts<LOGM, Pol>() == 16 ? FDE_PAIRED_MINB : FDE_PAIRED_MINB10;
-  return b * 128 / th > 0 ? b * 128 / th : 1;
-}
-
 template <int LOGM, class Pol, int EPI>
-__global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::THREADS,
-                                  paired_minb<LOGM, Pol>())
+__global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CTA_THREADS,
+                                  512 / PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CTA_THREADS)
     fft_line_kernel_paired(const Pol p) {
   pdl_enter();
   constexpr int P = paired_pts<LOGM, Pol>();
@@ -920,91 +967,112 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::TH
   using IO = LineIO<Pol, EPI>;
   constexpr int T = S::T, H = P / 2, R0 = S::R0, B0 = S::B0, NS0 = S::NS0;
   extern __shared__ __align__(16) double smem_all[];
-  // S::LPC lines per CTA in lockstep: thread tl of line slot ls
-  const int ls = threadIdx.x / T, tl = threadIdx.x - ls * T, warp = threadIdx.x >> 5;
-  double* const smem = smem_all + ls * S::LINE_DOUBLES;  // this line's buffers
-  double* const xbuf = smem + S::NBUF * 2 * S::BUF;  // next line's input (own slots only)
-  // the TMEM base address lands in the first exchange-buffer word (read into a
-  // register before any exchange): no static shared memory, so four CTAs fit
-  // a 196 KB carveout and the rest of the SM's L1 caches the spectral tables
-  uint32_t* const s_tbase = reinterpret_cast<uint32_t*>(smem_all);
+  // line group grp of the CTA; S::LPC lines per group in lockstep: thread tl
+  // of line slot ls.  Groups are the kernel's "virtual CTAs": vb of nvb.
+  const int grp = threadIdx.x / S::THREADS, tg = threadIdx.x - grp * S::THREADS;
+  const int ls = tg / T, tl = tg - ls * T, warp = threadIdx.x >> 5;
+  const int vb = grp * gridDim.x + blockIdx.x, nvb = gridDim.x * S::NG;  // balanced per SM
+  // Shared memory per line: the exchange slots only.  During the last
+  // inverse stage their first two planes of M doubles receive the first
+  // epilogue coefficient stream (plane 0) and the NEXT line's input (plane 1)
+  // by bulk copies that one thread issues (no LSU traffic, no registers).
+  // Four CTAs stay within the 164 KB shared-memory configuration, which leaves
+  // ~56 KB of L1 (tools/l1_probe.cu) for the stage twiddles and the stack;
+  // with a third 16 KB plane per CTA (228 KB configuration, no L1 to speak of)
+  // the n = 2047 apply measured 144 us against 134.
+  double* const smem = smem_all + (grp * S::LPC + ls) * S::LINE_DOUBLES;
+  double* const xin = smem + S::BUF;  // plane 1: where a line's input lands
+  uint64_t* const bars =
+      reinterpret_cast<uint64_t*>(smem_all + S::NG * S::LPC * S::LINE_DOUBLES);
+  uint64_t* const bar_x = bars + 2 * (grp * S::LPC + ls);  // input line landed
+  uint64_t* const bar_c = bar_x + 1;                       // coefficient stream landed
+  uint32_t* const s_tbase = reinterpret_cast<uint32_t*>(bars + 2 * S::NG * S::LPC);
   const int n = p.blk.n, nl = p.nlines();
   constexpr int LPC = S::LPC;
   // line of this slot in the CTA's group starting at `base` (clamped: a slot
   // past the last line recomputes it and stores nothing)
   auto line_of = [&](int base) { return base + ls < nl ? base + ls : nl - 1; };
-
-  // Persistent CTA: lines blockIdx.x, + gridDim.x, ...  Each thread copies the
-  // next line's input slots (its own positions) into xbuf while the current
-  // line is transformed, so only the first line waits for HBM.
-  auto prefetch_x = [&](int line) {
-#ifdef FDE_EXP_NOX
-    return;
-#endif
-    const IO io(p, line, 2 * tl);
-#pragma unroll
-    for (int s = 0; s < H; ++s) {
-      const int i0 = 2 * (tl + s * T), d = 2 * s * T;
-      cp_async8(xbuf + i0, io.xaddr(i0 < n ? d : 0), i0 < n ? 8 : 0);
-      cp_async8(xbuf + i0 + 1, io.xaddr(i0 + 1 < n ? d + 1 : 0), i0 + 1 < n ? 8 : 0);
-    }
-    cp_async_commit();
+  auto sx_of = [&](int line) { return (p.par + line * n) & 1; };
+  // 16-byte chunks of a line's virtual image; the input of the array's last
+  // line must not be read past its end (its odd tail element is loaded by the
+  // thread that owns it)
+  auto chunks_of = [&](int line, bool exact) {
+    const int nv = n + sx_of(line);
+    return (uint32_t)((exact && line == nl - 1) ? nv / 2 : (nv + 1) / 2);
   };
-#ifdef FDE_EXP_STAGGER
-  {
-    const int slot = blockIdx.x / 148;
-    for (int k = 0; k < slot; ++k) __nanosleep(FDE_EXP_STAGGER);
+  // Persistent groups: lines vb, + nvb, ...; thread 0 of a slot moves a
+  // line's input into plane 1 with one bulk copy.
+  auto issue_input = [&](int line) {
+    const uint32_t bytes = chunks_of(line, true) * 16;
+    const double* src = IO(p, line, sx_of(line)).input();
+    mbar_expect_tx(bar_x, bytes);
+    bulk_g2s(xin, src, bytes, bar_x);
+  };
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < 2 * S::NG * LPC; ++i) mbar_init(bars + i, 1);
+    fence_mbar_init();
   }
-#endif
   if (warp == 0) tmem_alloc<S::TCOLS_CTA>(s_tbase);
-  if (blockIdx.x * LPC < nl) prefetch_x(line_of(blockIdx.x * LPC));
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  const uint32_t tbase = *s_tbase;  // the first exchange write follows a barrier
-  if constexpr (S::NBUF != 1) __syncthreads();
+  const uint32_t tbase = *s_tbase;
+  if (tl == 0 && vb * LPC < nl) issue_input(line_of(vb * LPC));
   // this warp's lane quadrant, and its warpgroup's column range
   const uint32_t tq = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * S::TCOLS);
   const uint32_t tqy = tq, tqt = tq + 4 * P;                    // Qy, Qt column ranges
-  constexpr bool kStashX = IO::kKeepX && FDE_X_TMEM && (FDE_X_TMEM_JACOBI || EPI != EPI_JACOBI);
-  const uint32_t tqx = tqy + 4 * H;  // stashed row input (Qy columns past T x's)
-  const double* const ep0 = smem;            // staged epilogue operands (exchange buffer)
-  const double* const ep1 = smem + S::BUF;
+  uint32_t phase = 0;  // both mbarriers complete once per line
 
 #pragma unroll 1
-  for (int base = blockIdx.x * LPC; base < nl; base += gridDim.x * LPC) {
+  for (int base = vb * LPC; base < nl; base += nvb * LPC) {
     const int line = line_of(base);
     const bool live = base + ls < nl;  // uniform per line slot
-    const int next = base + gridDim.x * LPC;
-    const IO io(p, line, 2 * tl);
-#if FDE_L2_PREFETCH_PAIRED
-    // compile-time trip count (16 T >= M >= n): no loop-carried predicate to spill
-#pragma unroll
-    for (int i = 0; i < (S::M + 16 * T - 1) / (16 * T); ++i)
-      if ((tl + i * T) * 16 < n) p.prefetch(line, tl + i * T);
-#endif
-    // 1) z_m = x_2m + i x_2m+1, m = tl + s*T, from this thread's xbuf slots
-    //    (zero filled beyond n); then start the next line's copy
-    cp_async_wait_all();
+    const int next = base + nvb * LPC;
+    const int sx = sx_of(line);
+    const int nv = n + sx;
+    // 1) z_m = x'_2m + i x'_2m+1, m = tl + s*T, from the bulk-copied virtual
+    //    line (zero outside [sx, nv))
+    mbar_wait(bar_x, phase);
     double2 v[P];
+    {
+      const IO io(p, line, sx);
+      const bool tailfix = line == nl - 1 && (nv & 1);
 #pragma unroll
-    for (int s = 0; s < H; ++s) {
-      const double2 t = *reinterpret_cast<const double2*>(xbuf + 2 * (tl + s * T));
-      v[s] = t;
-      v[s + H] = make_double2(0.0, 0.0);
+      for (int s = 0; s < H; ++s) {
+        const int pv = 2 * (tl + s * T);
+        double2 t = *reinterpret_cast<const double2*>(xin + pv);
+        if (tailfix && pv == nv - 1) t.x = __ldcg(io.input() + pv);
+        v[s] = make_double2(pv >= sx && pv < nv ? t.x : 0.0, pv + 1 < nv ? t.y : 0.0);
+        v[s + H] = make_double2(0.0, 0.0);
+      }
+#if FDE_BULK_PF
+      if (tl == 0) {  // this line's operand streams and the next line's input -> L2
+        const uint32_t bytes = chunks_of(line, false) * 16;
+        bulk_prefetch_l2(io.staged(0), bytes);
+        bulk_prefetch_l2(io.staged(1), bytes);
+        io.prefetch_rest(chunks_of(line, true) * 16);
+        if (next < nl) {
+          const int ln = line_of(next);
+          bulk_prefetch_l2(IO(p, ln, sx_of(ln)).input(), chunks_of(ln, true) * 16);
+        }
+      }
+#endif
     }
-    if (!IO::kKeepX && next < nl) prefetch_x(line_of(next));
 
     // 2) forward transform; ends with this thread's paired slots in v
     double2 w1s[P];
-    int cur = 0;
-    PFwd<LOGM, P, 0, true>::run(v, smem, cur, tl, p.blk.twM, w1s);
+    double2* const xbuf = reinterpret_cast<double2*>(smem);  // exchange slots
+    PFwd<LOGM, P, 0, true>::run(v, xbuf, tl, p.blk.twM, w1s, [] {});
 
     // 3) spectral step (see fft_line_kernel): partners are in registers;
-    //    results go to tensor memory in groups of 4 slots
+    //    results go to tensor memory in groups of 4 slots.  With
+    //      P  = ar zr + bi mi,  Q  = br mr - ai zi,
+    //      P' = ar zi + bi mr,  Q' = ai zr - br mi      (a = a_k, b = b_k, m = Z[M-k])
+    //    Qy = (P + Q, P' + Q') and Qt = (P - Q, P' - Q'): 12 FP64 instructions per k.
     {
       const bool t0 = tl == 0;
-      const double4* abv = p.blk.ab;
+      const double2* abv = p.blk.ab;
 #pragma unroll
       for (int g = 0; g < P; g += 4) {
         double2 qy[4], qt[4];
@@ -1020,12 +1088,12 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::TH
           const double2 ca = make_double2(1.0 + k, 0.5), cb = make_double2(0.25, 0.125 * k);
 #else
           double2 ca, cb;
-          ld_ab(abv + k, ca, cb);
+          ld_ab<S::M>(abv, k, ca, cb);
 #endif
-          const double t1 = ca.x * z.x, t2 = ca.y * z.y, t3 = ca.x * z.y, t4 = ca.y * z.x;
-          const double u1 = cb.x * mr, u2 = cb.y * mi, u3 = cb.y * mr, u4 = cb.x * mi;
-          qy[c] = make_double2((t1 - t2) + (u1 + u2), (t3 + t4) + (u3 - u4));
-          qt[c] = make_double2((t1 + t2) + (u2 - u1), (t3 - t4) + (u3 + u4));
+          const double pr = ca.x * z.x + cb.y * mi, qr = cb.x * mr - ca.y * z.y;
+          const double pi = ca.x * z.y + cb.y * mr, qi = ca.y * z.x - cb.x * mi;
+          qy[c] = make_double2(pr + qr, pi + qi);
+          qt[c] = make_double2(pr - qr, pi - qi);
         }
         tmem_st4(tqy + 4 * g, qy);
         tmem_st4(tqt + 4 * g, qt);
@@ -1035,10 +1103,10 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::TH
 
     // 4) inverse of Qy -> T x (packed; its H output slots are parked in the Qy
     //    columns), then 5) inverse of Qt -> T^T x.  One copy of the inverse
-    //    code (instruction-cache footprint); both start on exchange buffer 0.
-    //    Once the second inverse's last stage has its inputs in registers, the
-    //    exchange buffer receives two epilogue operand streams (cp.async),
-    //    overlapped with that stage's butterflies.
+    //    code (instruction-cache footprint).  Once the second inverse's last
+    //    stage has its inputs in registers, the exchange buffer receives the
+    //    two epilogue coefficient streams (bulk copies), overlapped with that
+    //    stage's butterflies.
     const int n_inv = 2 + (n < 0);  // opaque trip count: ptxas keeps the loop rolled
 #pragma unroll 1
     for (int it = 0; it < n_inv; ++it) {
@@ -1054,43 +1122,18 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::TH
           for (int c = 0; c < 4; ++c) v[g + c] = t[c];
         }
       }
-      if constexpr (kStashX) {
-        // row pass: the line's own input moves from xbuf to the Qy columns
-        // the first inverse no longer needs (H slots from column 4H), so the
-        // next line's copy overlaps both inverses instead of waiting for the
-        // epilogue (each thread touches only its own xbuf slots)
-        if (it == 0) {
-#pragma unroll
-          for (int g = 0; g < H; g += 4) {
-            double2 t[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-              t[c] = *reinterpret_cast<const double2*>(xbuf + 2 * (tl + (g + c) * T));
-            tmem_st4(tqx + 4 * g, t);
-          }
-          if (next < nl) prefetch_x(line_of(next));
-        }
-      }
-      cur = 0;
       auto stage_epilogue = [&]() {
         if (it == 0) return;
-#ifdef FDE_EXP_NOEPI
-        return;
-#endif
-        __syncthreads();  // every thread has read its last-stage inputs
-#pragma unroll
-        for (int s = 0; s < H; ++s) {
-          const int i0 = 2 * (tl + s * T), d = 2 * s * T;
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const bool ok = i0 + e < n;
-            cp_async8(smem + i0 + e, io.staged(0, ok ? d + e : 0), ok ? 8 : 0);
-            cp_async8(smem + S::BUF + i0 + e, io.staged(1, ok ? d + e : 0), ok ? 8 : 0);
-          }
+        group_bar<S::THREADS>();  // every thread has read its last-stage inputs
+        if (tl == 0) {
+          const uint32_t bytes = chunks_of(line, false) * 16;
+          fence_proxy_async();
+          mbar_expect_tx(bar_c, bytes);
+          bulk_g2s(smem, IO(p, line, sx).staged(0), bytes, bar_c);
+          if (next < nl) issue_input(line_of(next));
         }
-        cp_async_commit();
       };
-      pinverse<LOGM, P>(v, smem, cur, tl, p.blk.twM, w1s, stage_epilogue);
+      pinverse<LOGM, P>(v, xbuf, tl, p.blk.twM, w1s, stage_epilogue);
       if (it == 0) {
 #pragma unroll
         for (int g = 0; g < H; g += 4) {
@@ -1103,70 +1146,38 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::TH
       }
     }
 
-    // 6) epilogue in groups of 4 slots (8 positions); own staged slots only.
-    //    Every operand of a group is fetched before any of its stores, with
-    //    out-of-range positions clamped to the thread's first position
-    //    (2 tl < n) and only the stores predicated: the global loads of a
-    //    group are all in flight together (a tail group fetched element by
-    //    element behind its own stores serialised one L2 latency per load).
-#if FDE_EPI_AHEAD
-    // group 0's global operands are in flight while the staged streams land
-    typename IO::Glob gn[8];
-    auto fetch_group = [&](int g) {
+    // 6) epilogue in groups of IO::G slots (pairs of positions): every global
+    //    operand of a group is in flight before any of its stores; the first
+    //    group's are issued before the wait for the staged streams.
+    {
+      const IO io(p, line, sx);
+      constexpr int G = IO::G;
+      typename IO::Glob gl[G];
+      auto fetch_group = [&](int g) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
-        gn[2 * c] = io.fetch_glob(i0 < n ? d : 0);
-        gn[2 * c + 1] = io.fetch_glob(i0 + 1 < n ? d + 1 : 0);
-      }
-    };
-    fetch_group(0);
-#endif
-    cp_async_wait_all();
+        for (int c = 0; c < G; ++c) gl[c] = io.fetch_glob(2 * (tl + (g + c) * T));
+      };
+      fetch_group(0);
+      mbar_wait(bar_c, phase);
 #pragma unroll
-    for (int g = 0; g < H; g += 4) {
-      double2 ty[4], tx[4];
-      tmem_ld4(tqy + 4 * g, ty);
-      if constexpr (kStashX) tmem_ld4(tqx + 4 * g, tx);
-      typename IO::Ops o[8];
-#if FDE_EPI_AHEAD
-      // later groups fetch at their top (fetching group g + 4 before group g
-      // is used spills ~230 B in the Jacobi instance: measured 2 % slower)
-      if (g > 0) fetch_group(g);
-      typename IO::Glob gc[8];
+      for (int g4 = 0; g4 < H; g4 += 4) {
+        double2 ty[4];
+        tmem_ld4(tqy + 4 * g4, ty);
 #pragma unroll
-      for (int c = 0; c < 8; ++c) gc[c] = gn[c];
-#endif
+        for (int g = g4; g < g4 + 4; g += G) {
+          if (g > 0) fetch_group(g);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int i0 = 2 * (tl + (g + c) * T);
-        [[maybe_unused]] const int d = 2 * (g + c) * T;
-        const double2 a = *reinterpret_cast<const double2*>(ep0 + i0);
-        const double2 b = *reinterpret_cast<const double2*>(ep1 + i0);
-        const double2 xv = kStashX       ? tx[c]
-                           : IO::kKeepX ? *reinterpret_cast<const double2*>(xbuf + i0)
-                                        : make_double2(0.0, 0.0);
-#ifdef FDE_EXP_NOEPI
-        o[2 * c] = typename IO::Ops{a.x, b.x};
-        o[2 * c + 1] = typename IO::Ops{a.y, b.y};
-#elif FDE_EPI_AHEAD
-        o[2 * c] = io.combine(gc[2 * c], a.x, b.x, xv.x);
-        o[2 * c + 1] = io.combine(gc[2 * c + 1], a.y, b.y, xv.y);
-#else
-        o[2 * c] = io.fetch_rest(i0 < n ? d : 0, a.x, b.x, xv.x);
-        o[2 * c + 1] = io.fetch_rest(i0 + 1 < n ? d + 1 : 0, a.y, b.y, xv.y);
-#endif
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int i0 = 2 * (tl + (g + c) * T), d = 2 * (g + c) * T;
-        if (live && i0 < n) io.finish(d, ty[c].x, v[g + c].x, o[2 * c]);
-        if (live && i0 + 1 < n) io.finish(d + 1, ty[c].y, v[g + c].y, o[2 * c + 1]);
+          for (int c = 0; c < G; ++c) {
+            const int pv = 2 * (tl + (g + c) * T);
+            const double2 a = *reinterpret_cast<const double2*>(smem + pv);
+            io.finish(pv, live, ty[g - g4 + c], v[g + c], a, gl[c]);
+          }
+        }
       }
     }
-    // row pass without the stash: the next line's input lands once this
-    // line's epilogue is done
-    if (IO::kKeepX && !kStashX && next < nl) prefetch_x(line_of(next));
+    phase ^= 1;
+    // the exchange slots are rewritten by the next line's first exchange,
+    // after the barrier that follows its input reads
   }
   tmem_fence_before();
   __syncthreads();
@@ -1306,62 +1317,96 @@ void launch_fft(const P& p, cudaStream_t s) {
 #define FDE_PAIRED 1
 #endif
 
-// Shared-memory carveout (percent of the 228 KB maximum): 85 % selects the
-// 196 KB configuration, which still holds four CTAs (4 x 49,152 B + 1 KB
-// reserved each) and leaves 60 KB of L1 for the spectral constants and
-// twiddles (measured 165 -> 160 us per n = 2047 apply against the maximum).
-#ifndef FDE_PAIRED_CARVEOUT
-#define FDE_PAIRED_CARVEOUT 85
+// Extra shared-memory carveout (percent) on top of what the resident CTAs
+// need; 0 leaves the most L1.
+#ifndef FDE_PAIRED_CARVEOUT_PAD
+#define FDE_PAIRED_CARVEOUT_PAD 0
 #endif
+// Whether the paired kernel's aligned I/O applies: every line-contiguous
+// stream's base address agrees modulo 16 bytes (then par = that parity in
+// doubles), and the virtual line of an odd row still fits the zero-padded
+// half (n + 1 <= M).  Otherwise the pass runs on fft_line_kernel.
+inline int common_parity(std::initializer_list<const void*> ptrs) {
+  int par = -1;
+  for (const void* q : ptrs) {
+    if (!q) continue;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(q);
+    if (a & 7) return -1;
+    const int b = (int)((a >> 3) & 1);
+    if (par >= 0 && b != par) return -1;
+    par = b;
+  }
+  return par;
+}
+inline int paired_parity(const XPass& p) {
+  return common_parity({p.x, p.dp, p.dm, p.q, p.out, p.epi == EPI_RHS ? p.src : nullptr,
+                        p.epi == EPI_RESID || p.epi == EPI_JACOBI ? p.b : nullptr,
+                        p.epi == EPI_JACOBI ? p.dinv : nullptr});
+}
+inline int paired_parity(const YPass& p) {
+  if (!p.xT) return -1;  // the bulk copy needs contiguous lines
+  return common_parity({p.x, p.epT, p.emT, p.qT ? p.q : nullptr});
+}
+
 template <int LOGM, class P, int EPI>
 void launch_paired_epi(const P& p, cudaStream_t s) {
   constexpr int PP = paired_pts<LOGM, P>();
   using S = PairedShape<LOGM, PP>;
-  static bool configured = false;
-  if (!configured) {
-    FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
-    // resident CTAs are register-bound; give shared memory the whole carveout
-    FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
-                                  cudaFuncAttributePreferredSharedMemoryCarveout,
-                                  FDE_PAIRED_CARVEOUT));
-    configured = true;
-  }
-  static int max_ctas = 0;  // resident CTAs on the device (persistent grid)
-  if (!max_ctas) {
-    // registers, shared memory and tensor-memory columns per SM, whichever
-    // binds (the occupancy API does not see the TMEM allocation)
-    int dev = 0, sms = 0, smem_sm = 0, smem_rsv = 0, regs_sm = 0;
-    FDE_CUDA(cudaGetDevice(&dev));
-    FDE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    FDE_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-    FDE_CUDA(cudaDeviceGetAttribute(&smem_rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev));
-    FDE_CUDA(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
-    cudaFuncAttributes fa{};
-    FDE_CUDA(cudaFuncGetAttributes(&fa, fft_line_kernel_paired<LOGM, P, EPI>));
-    const int regs_cta = ((fa.numRegs * 32 + 255) / 256 * 256) * (S::THREADS / 32);
-    int per_sm = regs_sm / regs_cta;
-    const int by_smem = smem_sm / (int)(S::SMEM + fa.sharedSizeBytes + smem_rsv);
-    const int by_tmem = 512 / S::TCOLS_CTA;
-    per_sm = per_sm < by_smem ? per_sm : by_smem;
-    per_sm = per_sm < by_tmem ? per_sm : by_tmem;
-    max_ctas = sms * (per_sm > 0 ? per_sm : 1);
+  // resident CTAs on the device (persistent grid) and the shared-memory
+  // carveout that just holds them: registers, tensor-memory columns and
+  // shared memory per SM, whichever binds (the occupancy API does not see
+  // the TMEM allocation).  What the carveout leaves of the SM's 256 KB is
+  // L1: it keeps the spectral constants (64 KB per block at M = 2048) and
+  // the twiddle tables resident across lines.
+  static std::mutex mu;
+  static std::map<int, int> ctas_of;  // per device
+  int dev = 0;
+  FDE_CUDA(cudaGetDevice(&dev));
+  int max_ctas = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = ctas_of.find(dev);
+    if (it == ctas_of.end()) {
+      int sms = 0, smem_sm = 0, smem_rsv = 0, regs_sm = 0;
+      FDE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      FDE_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+      FDE_CUDA(cudaDeviceGetAttribute(&smem_rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev));
+      FDE_CUDA(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
+      FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+      cudaFuncAttributes fa{};
+      FDE_CUDA(cudaFuncGetAttributes(&fa, fft_line_kernel_paired<LOGM, P, EPI>));
+      const int regs_cta = ((fa.numRegs * 32 + 255) / 256 * 256) * (S::CTA_THREADS / 32);
+      const int cta_smem = (int)(S::SMEM + fa.sharedSizeBytes) + smem_rsv;
+      int per_sm = regs_sm / regs_cta;
+      const int by_smem = smem_sm / cta_smem;
+      const int by_tmem = 512 / S::TCOLS_CTA;
+      per_sm = per_sm < by_smem ? per_sm : by_smem;
+      per_sm = per_sm < by_tmem ? per_sm : by_tmem;
+      if (per_sm < 1) per_sm = 1;
+      int carve = (per_sm * cta_smem * 100 + smem_sm - 1) / smem_sm + FDE_PAIRED_CARVEOUT_PAD;
+      if (carve > 100) carve = 100;
+      FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+      it = ctas_of.emplace(dev, sms * per_sm).first;
+    }
+    max_ctas = it->second;
   }
   const int groups = (lines_of(p) + S::LPC - 1) / S::LPC;
-  launch_k(fft_line_kernel_paired<LOGM, P, EPI>, groups < max_ctas ? groups : max_ctas, S::THREADS,
-                                         S::SMEM, s, p);
+  const int ctas = (groups + S::NG - 1) / S::NG;
+  launch_k(fft_line_kernel_paired<LOGM, P, EPI>, ctas < max_ctas ? ctas : max_ctas,
+           S::CTA_THREADS, S::SMEM, s, p);
   FDE_LAUNCH_CHECK();
 }
 
 template <int LOGM, class P>
-void launch_paired(const P& p, cudaStream_t s) {
+void launch_paired(const P& p0, cudaStream_t s) {
+  P p = p0;
+  p.par = paired_parity(p);
+  if (p.par < 0 || p.blk.n + 1 > (1 << LOGM)) return launch_fft<LOGM>(p0, s);
   if constexpr (std::is_same<P, YPass>::value) {
-    switch ((p.xT ? 1 : 0) | (p.qT ? 2 : 0)) {
-      case 1: return launch_paired_epi<LOGM, P, 1>(p, s);
-      case 2: return launch_paired_epi<LOGM, P, 2>(p, s);
-      case 3: return launch_paired_epi<LOGM, P, 3>(p, s);
-      default: return launch_paired_epi<LOGM, P, 0>(p, s);
-    }
+    if (p.qT) return launch_paired_epi<LOGM, P, 2>(p, s);
+    return launch_paired_epi<LOGM, P, 0>(p, s);
   } else {
     switch (p.epi) {
       case EPI_RHS: return launch_paired_epi<LOGM, P, EPI_RHS>(p, s);

@@ -35,8 +35,8 @@ constexpr int kDirectMax = 32;  // n <= this: direct Toeplitz product
 struct LineBlockDev {
   int n;                 // line length
   int logM;              // FFT path: M = 2^logM = L/2; 0 -> direct path
-  const double4* ab;     // spectral constants: (a_k, b_k) at index k, k < M (operator.cu)
-  const double2* twM;    // exp(-2 pi i k / M), k < M
+  const double2* ab;     // spectral constants, compact: a_k at k (k < M), b_c at M + c (c <= M/2) (operator.cu)
+  const double2* twM;    // stage twiddles, compact: exp(-2 pi i j / Q), j < Q/2, at Q/2 + j (Q = 2..M)
   const double* col;     // first column, n entries (direct path)
   const double* row;     // first row, n entries (direct path)
 };
@@ -93,6 +93,7 @@ struct YPass {
   double c;           // sign * s_over_r
   double* q;          // Q[i + j * n1], or Q transposed (Q[i * n2 + j]) when qT is set
   int qT;
+  int par = 0;        // set by the launcher: common base-address parity (line_conv.cu)
   __device__ __forceinline__ int nlines() const { return n1; }
   __device__ __forceinline__ double load(int line, int pos) const {
     return xT ? x[(size_t)line * n2 + pos] : x[(size_t)pos * n1 + line];
@@ -143,6 +144,7 @@ struct XPass {
   double omega;
   const double* src;   // EPI_RHS
   double src_scale;
+  int par = 0;         // set by the launcher: common base-address parity (line_conv.cu)
   __device__ __forceinline__ int nlines() const { return n2; }
   __device__ __forceinline__ double load(int line, int pos) const {
     return x[(size_t)line * n1 + pos];

@@ -89,8 +89,14 @@ const TwiddleTables& twiddles(int logM) {
   auto& slot = cache[logM];
   if (!slot) {
     const size_t M = size_t(1) << logM;
-    std::vector<double2> tm(M);
-    for (size_t k = 0; k < M; ++k) tm[k] = unit_root(k, M);
+    // compact per-stage layout: exp(-2 pi i j / Q), j < Q / 2, at Q / 2 + j for
+    // every power of two Q <= M.  A stage with NS butterflies per group and
+    // radix R reads the NS contiguous entries from NS R / 2, so the twiddles a
+    // line kernel touches cover a few KB of L1 lines instead of strided
+    // sectors all over a 16 M-byte table.
+    std::vector<double2> tm(M, make_double2(1.0, 0.0));
+    for (size_t Q = 2; Q <= M; Q <<= 1)
+      for (size_t j = 0; j < Q / 2; ++j) tm[Q / 2 + j] = unit_root(j, Q);
     auto t = std::make_unique<TwiddleTables>();
     t->twM.upload(tm.data(), M);
     slot = std::move(t);
@@ -127,7 +133,9 @@ ToeplitzDev::ToeplitzDev(std::vector<double> first_col, std::vector<double> firs
   // (line_conv.cu): with S~ = S / (2L), a = S~[k], b = conj(S~[M-k]),
   // W = exp(-2 pi i k / L) = cw + i sw:
   //   a_k = 2 (a + b + sw (a - b)),  b_k = 2 i cw (a - b).
-  std::vector<double4> ab(M);
+  // Compact layout: a_k at index k (k < M); b_c at M + c for c <= M / 2 only,
+  // because b_{M-k} = -conj(b_k) (cw flips sign, a and conj(b) swap).
+  std::vector<double2> ab(M + M / 2 + 2, make_double2(0.0, 0.0));
   const long double sc = 1.0L / (2.0L * (long double)L_);
   for (size_t k = 0; k < M; ++k) {
     const cld a = c[k] * sc, b = std::conj(c[M - k] * sc);
@@ -135,10 +143,10 @@ ToeplitzDev::ToeplitzDev(std::vector<double> first_col, std::vector<double> firs
     const long double cw = cosl(ang), sw = -sinl(ang);
     const cld ak = 2.0L * (a + b + sw * (a - b));
     const cld bk = 2.0L * cld(0.0L, cw) * (a - b);
-    // (a_k, b_k) interleaved: one 32-byte load per k in the line kernels
-    ab[k] = double4{(double)ak.real(), (double)ak.imag(), (double)bk.real(), (double)bk.imag()};
+    ab[k] = make_double2((double)ak.real(), (double)ak.imag());
+    if (k <= M / 2) ab[M + k] = make_double2((double)bk.real(), (double)bk.imag());
   }
-  spec_ = std::make_shared<DevBuf<double4>>();
+  spec_ = std::make_shared<DevBuf<double2>>();
   spec_->upload(ab.data(), ab.size());
 }
 
@@ -308,7 +316,9 @@ void StructuredOp::sync_host(cudaStream_t s) {
 #define FDE_XT_MIN 512  // measured: 128 or 256 (-0.4 to -1 %), 1024 (-0.3 %) slower
 #endif
 bool StructuredOp::maps_input() const {
-  return ay_.dev().logM && n1_ >= FDE_XT_MIN && transpose_columns_;
+  // (the paired kernels, logM >= 10, bulk-copy contiguous lines: always transposed)
+  const int lm = ay_.dev().logM;
+  return lm && (lm >= 10 || (n1_ >= FDE_XT_MIN && transpose_columns_));
 }
 
 void StructuredOp::run(const double* x, double* out, double sign, int epi, const EpiArgs& e,

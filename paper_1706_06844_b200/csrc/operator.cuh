@@ -44,7 +44,7 @@ class ToeplitzDev {
   size_t n_ = 0, L_ = 0;
   int logM_ = 0;
   std::vector<double> col_, row_;
-  std::shared_ptr<DevBuf<double4>> spec_;  // per-k spectral constants
+  std::shared_ptr<DevBuf<double2>> spec_;  // per-k spectral constants
   std::shared_ptr<DevBuf<double>> dcol_, drow_;
 };
 

@@ -95,6 +95,55 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, double2 (&v)[16]) {
 }  // namespace fde_b200
 
 namespace fde_b200 {
+// ---- bulk asynchronous copies (TMA engine, SASS UBLKCP) + mbarriers --------
+// One thread moves a whole line global -> shared with a single instruction;
+// completion is counted in bytes on an mbarrier every consumer waits on.  No
+// LSU instruction is issued for the data (the per-thread 8-byte cp.async
+// copies these replace cost 48 LSU instructions per thread per line).
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// orders this thread's earlier generic-proxy shared-memory accesses before
+// later async-proxy (bulk copy) accesses
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "FDE_MBAR_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra FDE_MBAR_DONE;\n"
+      "bra FDE_MBAR_WAIT;\n"
+      "FDE_MBAR_DONE:\n"
+      "}" ::"r"(smem_addr_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared, `bytes` a positive multiple of 16, both addresses 16-byte aligned
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_addr_u32(bar))
+      : "memory");
+}
+// warm L2 with `bytes` (multiple of 16) from a 16-byte aligned address
+__device__ __forceinline__ void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gsrc), "r"(bytes) : "memory");
+}
+
 // ---- cp.async (LDGSTS) helpers: global -> shared without registers --------
 // 8-byte copy; src_bytes = 0 zero-fills the destination (address must still be valid)
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, int src_bytes) {

@@ -33,9 +33,13 @@ typedef enum {
   FDE_ENOMEM = 4
 } fde_status;
 
-/* PrecondKind (proj/include/fde/precond.hpp:18; p2_exact and mgm_galerkin are not offered) and mg::CoarseSolve
- * (proj/include/fde/multigrid.hpp:95) */
-enum { FDE_PRECOND_NONE = 0, FDE_PRECOND_P2 = 1, FDE_PRECOND_MGM = 2 };
+/* PrecondKind (proj/include/fde/precond.hpp:18; numbered none, p2, mgm, p2-exact, mgm-galerkin here,
+ * see fde_precond_create) and mg::CoarseSolve (proj/include/fde/multigrid.hpp:95).
+ * p2-exact is a single-CTA shared-memory banded solve: at most 25,600 unknowns with half bandwidth
+ * <= 256 (FDE_EINVAL beyond that; the reference's Eigen SparseLU has no such limit).  mgm-galerkin
+ * keeps the reference's own guard n1, n2 <= 128 (precond.cpp:121-123). */
+enum { FDE_PRECOND_NONE = 0, FDE_PRECOND_P2 = 1, FDE_PRECOND_MGM = 2, FDE_PRECOND_P2_EXACT = 3,
+       FDE_PRECOND_MGM_GALERKIN = 4 };
 enum { FDE_COARSE_LU = 0, FDE_COARSE_SWEEPS = 1, FDE_COARSE_NONE = 2 };
 
 const char* fde_last_error(void);
@@ -296,6 +300,10 @@ int fde_dot(size_t n, const double* x, const double* y, double* out_dev, int sqr
 
 /* Number of kernels this library has launched since load (instrumentation). */
 unsigned long long fde_kernel_launches(void);
+/* Measured FP64 FMA throughput of the current device in TFLOP/s (a pure DFMA
+ * kernel, best of three timed launches): the roofline denominator of the
+ * FP64-issue-bound line kernels, taken in the reporting run. */
+int fde_fp64_peak(double* tflops, void* stream);
 
 #ifdef __cplusplus
 }

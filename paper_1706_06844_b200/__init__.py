@@ -80,6 +80,7 @@ _SIGS = {
     "fde_last_error": (ctypes.c_char_p, []),
     "fde_abi_version": (_c_int, []),
     "fde_kernel_launches": (ctypes.c_ulonglong, []),
+    "fde_fp64_peak": (_c_int, [ctypes.POINTER(_c_dbl), _c_vp]),
     "fde_wsgd_weights": (_c_int, [_c_dbl, _c_size, _c_int, _P, _P]),
     "fde_op_create": (_c_int, [_c_size, _c_size, _c_dbl, _c_dbl] + [_P] * 8 + [ctypes.POINTER(_c_vp)]),
     "fde_op_create_fractional": (_c_int, [_c_size, _c_size, _c_dbl, _c_dbl, _c_dbl, _c_dbl, _c_int]
@@ -201,6 +202,13 @@ def _check(rc: int) -> None:
 
 def kernel_launches() -> int:
     return int(load_library().fde_kernel_launches())
+
+
+def fp64_peak_tflops() -> float:
+    """Measured DFMA throughput of the current device (TFLOP/s)."""
+    v = _c_dbl(0.0)
+    _check(load_library().fde_fp64_peak(ctypes.byref(v), None))
+    return float(v.value)
 
 
 # ------------------------------------------------------------------ tensors

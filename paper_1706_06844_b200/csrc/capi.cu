@@ -211,6 +211,12 @@ extern "C" {
 const char* fde_last_error(void) { return g_error.c_str(); }
 int fde_abi_version(void) { return FDE_B200_ABI_VERSION; }
 unsigned long long fde_kernel_launches(void) { return g_kernel_launches.load(); }
+int fde_fp64_peak(double* tflops, void* stream) {
+  return guard([&] {
+    need(tflops != nullptr, "null argument");
+    *tflops = fp64_peak_tflops(stream_of(stream));
+  });
+}
 
 int fde_wsgd_weights(double gamma, size_t K, int pq, double* g, double* w) {
   return guard([&] {
@@ -522,6 +528,7 @@ int fde_gmres(fde_op a, fde_precond m, const fde_solver_config* cfg, const doubl
               double* x, fde_krylov_result* res, void* stream) {
   return guard([&] {
     need(a && cfg && b && x, "null argument");
+    need(b != x, "the solution must not alias the right-hand side (x is zeroed first)");
     SolverConfig c{cfg->tol, cfg->restart, cfg->max_outer};
     need(c.restart > 0 && c.tol > 0.0, "invalid solver configuration");
     KrylovWorkspace& ws = workspace_for(a->ws, a->op->size(), c.restart);
@@ -533,7 +540,9 @@ int fde_bicgstab(fde_op a, fde_precond m, const fde_solver_config* cfg, const do
                  double* x, fde_krylov_result* res, void* stream) {
   return guard([&] {
     need(a && cfg && b && x, "null argument");
+    need(b != x, "the solution must not alias the right-hand side (x is zeroed first)");
     SolverConfig c{cfg->tol, cfg->restart, cfg->max_outer};
+    need(c.tol > 0.0, "invalid solver configuration");
     KrylovWorkspace& ws = workspace_for(a->ws, a->op->size(), c.restart);
     fill_result(ws.bicgstab(*a->op, m ? m->pc.get() : nullptr, c, b, x, stream_of(stream)),
                 res);
@@ -642,8 +651,11 @@ int fde_march_step(fde_march h, const double* source, int source_mode, void* str
     } else {
       throw InvalidArgument("source_mode must be 0, 1, 2 or 3");
     }
-    // the solve overwrites h->x: a pending D2H of that buffer must finish first
-    if (h->cs && h->d2h_buf == h->x.get()) FDE_CUDA(cudaStreamWaitEvent(s, h->ev_d2h, 0));
+    // the solve overwrites h->x: any solution copy still in flight must finish
+    // first.  ev_d2h is the LAST copy on the (in-order) copy stream, so it
+    // covers every earlier one too -- two back-to-back asynchronous reads leave
+    // both u^m buffers pending, not just the most recent.
+    if (h->cs && h->d2h_buf) FDE_CUDA(cudaStreamWaitEvent(s, h->ev_d2h, 0));
     // assemble_rhs (problem.cpp:73-89): b = apply_rhs(u) + 2 hx^alpha v, fused
     EpiArgs e;
     e.src = src;

@@ -9,9 +9,9 @@
 // reference's `--n <= 4096` cap becomes the line-kernel limit (n <= 4096 per
 // direction).  Extensions: --config K runs BASELINE configuration K (1..5,
 // seeded sources), --solver bicgstab, --seed.  Exit codes
-// follow the reference: 0 ok, 1 some
-// step did not converge, 2 usage error; library failures print
-// fde_last_error() and exit 3.
+// follow the reference (proj/src/cli.cpp:135,473-476): 0 ok, 1 some step did
+// not converge or the run failed with an exception (library failures print
+// fde_last_error()), 2 usage error.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -392,9 +392,9 @@ int main(int argc, char** argv) {
     return 2;
   } catch (const LibError& e) {
     std::fprintf(stderr, "error: %s\n", e.what());
-    return 3;
+    return 1;
   } catch (const std::exception& e) {
     std::fprintf(stderr, "error: %s\n", e.what());
-    return 3;
+    return 1;
   }
 }

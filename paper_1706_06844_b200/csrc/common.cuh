@@ -4,6 +4,8 @@
 
 #include <atomic>
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -35,6 +37,33 @@ extern std::atomic<unsigned long long> g_kernel_launches;
     ::fde_b200::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \
     ::fde_b200::cuda_check(cudaGetLastError(), "kernel launch");            \
   } while (0)
+
+// ---- one-time per-device setup --------------------------------------------
+// Kernel attributes (opt-in shared memory, carveout) and occupancy-derived
+// grids belong to a device, not to the process: a second GPU touched by the
+// same process needs its own setup.  DeviceCache<T> maps the current device
+// to a value built on first use.
+inline int current_device() {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  return dev;
+}
+template <class T>
+class DeviceCache {
+ public:
+  template <class Make>
+  T& get(Make&& make) {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lock(mu_);
+    auto it = vals_.find(dev);
+    if (it == vals_.end()) it = vals_.emplace(dev, make(dev)).first;
+    return it->second;
+  }
+
+ private:
+  std::mutex mu_;
+  std::map<int, T> vals_;
+};
 
 // ---- programmatic dependent launch ---------------------------------------
 // Every kernel is launched with programmatic stream serialization and opens

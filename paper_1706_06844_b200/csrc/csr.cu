@@ -288,12 +288,12 @@ BandedLu::BandedLu(const Csr& a, size_t bw) : n_(a.rows), bw_(bw) {
 }
 
 void BandedLu::solve(const double* r, double* z, cudaStream_t s) const {
-  static bool configured = false;
-  if (!configured) {
+  static DeviceCache<bool> configured;  // per device
+  configured.get([](int) {
     FDE_CUDA(cudaFuncSetAttribute(k_band_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   200 * 1024));
-    configured = true;
-  }
+    return true;
+  });
   launch_k(k_band_solve, 1, 32, n_ * sizeof(double), s, n_, (int)bw_, d_band_.get(), r, z);
   FDE_LAUNCH_CHECK();
 }

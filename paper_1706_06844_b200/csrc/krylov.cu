@@ -22,30 +22,6 @@ void copy_scale(size_t n, double a, const double* x, double* y, cudaStream_t s) 
   FDE_LAUNCH_CHECK();
 }
 
-// p = r + beta (p - omega v)     (BiCGSTAB direction update)
-__global__ void k_bicg_p(size_t n, double beta, double omg, const double* __restrict__ r,
-                         const double* __restrict__ v, double* __restrict__ p) {
-  pdl_enter();
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x)
-    p[i] = r[i] + beta * (p[i] - omg * v[i]);
-}
-// s = r - alpha v
-__global__ void k_axpy2(size_t n, double a, const double* __restrict__ x,
-                        const double* __restrict__ y, double* __restrict__ out) {
-  pdl_enter();
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x)
-    out[i] = y[i] - a * x[i];
-}
-// x += alpha p + omega s
-__global__ void k_bicg_x(size_t n, double alpha, double omg, const double* __restrict__ p,
-                         const double* __restrict__ sv, double* __restrict__ x) {
-  pdl_enter();
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x)
-    x[i] += alpha * p[i] + omg * sv[i];
-}
 // Small scalar transfers between device scratch and the pinned host staging
 // (UVA-mapped): one tiny kernel instead of a DMA copy, so the solver's
 // per-iteration round trip never queues behind bulk host copies running on
@@ -72,11 +48,6 @@ void copy_vec(size_t n, const double* x, double* y, cudaStream_t s) {
   if (blocks > 148 * 8) blocks = 148 * 8;
   launch_k(k_copy, blocks ? blocks : 1, 256, 0, s, n, x, y);
   FDE_LAUNCH_CHECK();
-}
-
-int nblocks(size_t n) {
-  int b = (int)((n + 255) / 256);
-  return b > 148 * 8 ? 148 * 8 : (b ? b : 1);
 }
 
 // back_substitute (krylov.cpp:19-30)
@@ -426,26 +397,33 @@ KrylovResult KrylovWorkspace::bicgstab(const StructuredOp& a, const Precond* m,
     precondition(m, tmp2, out, s);
     return nrm2_host(out, s) / norm_b;
   };
-  double rho = 1.0, alpha = 1.0, omg = 1.0;
+  // Fused iteration: every reduction lands in the device scalar block sc,
+  // alpha / omega / beta are formed there, and the host reads the block twice
+  // per iteration (after the half step and after the full step) for the
+  // breakdown and convergence tests -- the same tests, in the same order, as
+  // the restatement in oracle/fde_oracle.c.
+  double* const sc = dsc_.get();
+  int rho_cur = BICG_RHO_A;
+  red_.dot(n, rh, r, sc + rho_cur, s, false);
+  fetch(BICG_SLOTS, s);
+  double rho_host = hsc_[rho_cur];
   for (size_t it = 0; it < max_it; ++it) {
-    const double rho_new = dot_host(rh, r, s);
-    if (rho_new == 0.0) break;
+    if (rho_host == 0.0) break;
+    const int rho_old = rho_cur ^ 1;  // the previous iteration's <rh, r>
     if (it == 0) {
       copy_vec(n, r, p, s);
     } else {
-      const double beta = (rho_new / rho) * (alpha / omg);
-      launch_k(k_bicg_p, nblocks(n), 256, 0, s, n, beta, omg, r, v, p);
-      FDE_LAUNCH_CHECK();
+      red_.bicg_p(n, r, v, p, sc, rho_cur, rho_old, s);
     }
     a.apply(p, tmp, s);
     precondition(m, tmp, v, s);
-    const double rv = dot_host(rh, v, s);
-    if (rv == 0.0) break;
-    alpha = rho_new / rv;
-    launch_k(k_axpy2, nblocks(n), 256, 0, s, n, alpha, v, r, sv);  // s = r - alpha v
-    FDE_LAUNCH_CHECK();
+    red_.dot(n, rh, v, sc + BICG_RV, s, false);
+    red_.bicg_s(n, r, v, sv, sc, rho_cur, s);  // alpha, s = r - alpha v, ||s||
+    fetch(BICG_SLOTS, s);                      // host read 1 of 2
+    if (hsc_[BICG_RV] == 0.0) break;
+    const double alpha = hsc_[BICG_ALPHA];
     ++res.total_iterations;
-    const double srel = nrm2_host(sv, s) / norm_b;
+    const double srel = hsc_[BICG_NS] / norm_b;
     if (srel <= cfg.tol) {  // half step: verify x + alpha p
       double* trial = trial_.get();
       copy_vec(n, x, trial, s);
@@ -460,14 +438,14 @@ KrylovResult KrylovWorkspace::bicgstab(const StructuredOp& a, const Precond* m,
     }
     a.apply(sv, tmp, s);
     precondition(m, tmp, tv, s);
-    const double tt = dot_host(tv, tv, s);
-    omg = tt > 0.0 ? dot_host(tv, sv, s) / tt : 0.0;
-    launch_k(k_bicg_x, nblocks(n), 256, 0, s, n, alpha, omg, p, sv, x);
-    FDE_LAUNCH_CHECK();
-    launch_k(k_axpy2, nblocks(n), 256, 0, s, n, omg, tv, sv, r);  // r = s - omega t
-    FDE_LAUNCH_CHECK();
-    rho = rho_new;
-    const double rel = nrm2_host(r, s) / norm_b;
+    red_.bicg_tt(n, tv, sv, sc, s);
+    // omega, x += alpha p + omega s, r = s - omega t, ||r||, next <rh, r>
+    red_.bicg_xr(n, p, sv, tv, rh, x, r, sc, rho_old, s);
+    fetch(BICG_SLOTS, s);  // host read 2 of 2
+    rho_cur = rho_old;
+    rho_host = hsc_[rho_cur];
+    const double omg = hsc_[BICG_OMEGA];
+    const double rel = hsc_[BICG_NR] / norm_b;
     res.residual_history.push_back(rel);
     if (rel <= cfg.tol) {
       if (true_res(x, tmp) <= cfg.tol) {

@@ -10,8 +10,6 @@
 // the other powers come from a depth-4 product tree (the FP64 pipe has the
 // headroom, the L1/shared-memory pipe does not).
 #include <initializer_list>
-#include <map>
-#include <mutex>
 #include <type_traits>
 
 #include "line_conv.cuh"
@@ -948,6 +946,9 @@ struct LineIO<XPass, EPI> {
 #ifndef FDE_PAIRED8
 #define FDE_PAIRED8 0  // M = 256, 8 points/thread, 4 lines per CTA: measured slower (V-cycle +5 %)
 #endif
+#ifndef FDE_SPEC_GROUP
+#define FDE_SPEC_GROUP 4  // slots per tensor-memory store in the spectral step
+#endif
 #ifndef FDE_BULK_PF
 #define FDE_BULK_PF 1  // L2 bulk prefetch of the line's operand streams at line start
 #endif
@@ -1022,10 +1023,13 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CT
   // this warp's lane quadrant, and its warpgroup's column range
   const uint32_t tq = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * S::TCOLS);
   const uint32_t tqy = tq, tqt = tq + 4 * P;                    // Qy, Qt column ranges
-  uint32_t phase = 0;  // both mbarriers complete once per line
-
+  // both mbarriers complete once per line: their phase parity rides in bit 30
+  // of the loop counter (one loop-carried register instead of two; a spilled
+  // parity word cost an exposed local-memory load before every wait)
 #pragma unroll 1
-  for (int base = vb * LPC; base < nl; base += nvb * LPC) {
+  for (int st = vb * LPC; (st & 0x3fffffff) < nl; st = (st + nvb * LPC) ^ 0x40000000) {
+    const int base = st & 0x3fffffff;
+    const uint32_t phase = (uint32_t)st >> 30;
     const int line = line_of(base);
     const bool live = base + ls < nl;  // uniform per line slot
     const int next = base + nvb * LPC;
@@ -1074,29 +1078,30 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CT
       const bool t0 = tl == 0;
       const double2* abv = p.blk.ab;
 #pragma unroll
-      for (int g = 0; g < P; g += 4) {
-        double2 qy[4], qt[4];
+      for (int g = 0; g < P; g += FDE_SPEC_GROUP) {
+        double2 qy[FDE_SPEC_GROUP], qt[FDE_SPEC_GROUP];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < FDE_SPEC_GROUP; ++c) {
           const int s = g + c, q = s % B0, r = s / B0;
           const int k = paired_bfly<B0, T>(tl, q) + r * NS0;
           const double2 z = v[s];
           const double2 zm0 = v[partner_slot<B0, R0>(s, true)];
           const double2 zm1 = v[partner_slot<B0, R0>(s, false)];
           const double mr = t0 ? zm0.x : zm1.x, mi = t0 ? zm0.y : zm1.y;
-#ifdef FDE_EXP_NOAB
-          const double2 ca = make_double2(1.0 + k, 0.5), cb = make_double2(0.25, 0.125 * k);
-#else
           double2 ca, cb;
           ld_ab<S::M>(abv, k, ca, cb);
-#endif
           const double pr = ca.x * z.x + cb.y * mi, qr = cb.x * mr - ca.y * z.y;
           const double pi = ca.x * z.y + cb.y * mr, qi = ca.y * z.x - cb.x * mi;
           qy[c] = make_double2(pr + qr, pi + qi);
           qt[c] = make_double2(pr - qr, pi - qi);
         }
+#if FDE_SPEC_GROUP == 4
         tmem_st4(tqy + 4 * g, qy);
         tmem_st4(tqt + 4 * g, qt);
+#else
+        tmem_st2(tqy + 4 * g, qy);
+        tmem_st2(tqt + 4 * g, qt);
+#endif
       }
     }
     tmem_wait_st();
@@ -1175,7 +1180,6 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CT
         }
       }
     }
-    phase ^= 1;
     // the exchange slots are rewritten by the next line's first exchange,
     // after the barrier that follows its input reads
   }
@@ -1289,20 +1293,17 @@ int lines_of(const P& p) {
 template <int LOGM, class P>
 void launch_fft(const P& p, cudaStream_t s) {
   using S = FftShape<LOGM>;
-  static bool configured = false;  // per template instance
-  if (!configured) {
+  // per template instance and device: opt-in shared memory, SM count
+  static DeviceCache<int> sm_count;
+  const int sms = sm_count.get([](int dev) {
     FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel<LOGM, P>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
-    configured = true;
-  }
+    int n = 0;
+    FDE_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    return n;
+  });
   // spread small levels over the SMs: fewer lines per CTA until the grid
   // covers two waves (CTAs stay a whole number of warps)
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    FDE_CUDA(cudaGetDevice(&dev));
-    FDE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
   const int lines = lines_of(p);
   int lpb = S::LPB;
   const int min_lpb = S::T >= 32 ? 1 : 32 / S::T;
@@ -1358,40 +1359,31 @@ void launch_paired_epi(const P& p, cudaStream_t s) {
   // the TMEM allocation).  What the carveout leaves of the SM's 256 KB is
   // L1: it keeps the spectral constants (64 KB per block at M = 2048) and
   // the twiddle tables resident across lines.
-  static std::mutex mu;
-  static std::map<int, int> ctas_of;  // per device
-  int dev = 0;
-  FDE_CUDA(cudaGetDevice(&dev));
-  int max_ctas = 0;
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    auto it = ctas_of.find(dev);
-    if (it == ctas_of.end()) {
-      int sms = 0, smem_sm = 0, smem_rsv = 0, regs_sm = 0;
-      FDE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      FDE_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
-      FDE_CUDA(cudaDeviceGetAttribute(&smem_rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev));
-      FDE_CUDA(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
-      FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
-      cudaFuncAttributes fa{};
-      FDE_CUDA(cudaFuncGetAttributes(&fa, fft_line_kernel_paired<LOGM, P, EPI>));
-      const int regs_cta = ((fa.numRegs * 32 + 255) / 256 * 256) * (S::CTA_THREADS / 32);
-      const int cta_smem = (int)(S::SMEM + fa.sharedSizeBytes) + smem_rsv;
-      int per_sm = regs_sm / regs_cta;
-      const int by_smem = smem_sm / cta_smem;
-      const int by_tmem = 512 / S::TCOLS_CTA;
-      per_sm = per_sm < by_smem ? per_sm : by_smem;
-      per_sm = per_sm < by_tmem ? per_sm : by_tmem;
-      if (per_sm < 1) per_sm = 1;
-      int carve = (per_sm * cta_smem * 100 + smem_sm - 1) / smem_sm + FDE_PAIRED_CARVEOUT_PAD;
-      if (carve > 100) carve = 100;
-      FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
-                                    cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-      it = ctas_of.emplace(dev, sms * per_sm).first;
-    }
-    max_ctas = it->second;
-  }
+  static DeviceCache<int> resident;
+  const int max_ctas = resident.get([](int dev) {
+    int sms = 0, smem_sm = 0, smem_rsv = 0, regs_sm = 0;
+    FDE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FDE_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+    FDE_CUDA(cudaDeviceGetAttribute(&smem_rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev));
+    FDE_CUDA(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
+    FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+    cudaFuncAttributes fa{};
+    FDE_CUDA(cudaFuncGetAttributes(&fa, fft_line_kernel_paired<LOGM, P, EPI>));
+    const int regs_cta = ((fa.numRegs * 32 + 255) / 256 * 256) * (S::CTA_THREADS / 32);
+    const int cta_smem = (int)(S::SMEM + fa.sharedSizeBytes) + smem_rsv;
+    int per_sm = regs_sm / regs_cta;
+    const int by_smem = smem_sm / cta_smem;
+    const int by_tmem = 512 / S::TCOLS_CTA;
+    per_sm = per_sm < by_smem ? per_sm : by_smem;
+    per_sm = per_sm < by_tmem ? per_sm : by_tmem;
+    if (per_sm < 1) per_sm = 1;
+    int carve = (per_sm * cta_smem * 100 + smem_sm - 1) / smem_sm + FDE_PAIRED_CARVEOUT_PAD;
+    if (carve > 100) carve = 100;
+    FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
+                                  cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    return sms * per_sm;
+  });
   const int groups = (lines_of(p) + S::LPC - 1) / S::LPC;
   const int ctas = (groups + S::NG - 1) / S::NG;
   launch_k(fft_line_kernel_paired<LOGM, P, EPI>, ctas < max_ctas ? ctas : max_ctas,

@@ -169,6 +169,7 @@ Hierarchy::Hierarchy(std::vector<LevelOp> levels, std::vector<std::pair<size_t, 
       inv[i] = 1.0 / d[i];
     }
     dinv_[l].upload(inv.data(), inv.size());
+    if (levels_[l].sop) levels_[l].sop->freeze();  // 1/diag, inv_r, s/r are baked in from here on
     r_[l].alloc(d.size());
     if (l > 0) {
       bc_[l].alloc(d.size());

@@ -219,6 +219,9 @@ void StructuredOp::upload() {
 }
 
 void StructuredOp::scale(double s) {
+  if (frozen_)
+    throw InvalidArgument("scale(): the operator is a level of a multigrid hierarchy "
+                          "(scale it before building the hierarchy)");
   scales_.push_back(s);
   inv_r_ *= s;
   s_over_r_ *= s;

@@ -92,8 +92,11 @@ class StructuredOp {
   void apply_rhs(const double* x, double* y, cudaStream_t s) const {
     run(x, y, -1.0, EPI_STORE, EpiArgs{}, s);
   }
-  // structured.cpp:154-162
+  // structured.cpp:154-162.  Rejected once a hierarchy holds the operator:
+  // its one-launch coarse tail and the captured V-cycle graphs bake in inv_r,
+  // s/r and 1/diag, so a later scale() would leave them silently stale.
   void scale(double s);
+  void freeze() const { frozen_ = true; }
 
   // Per-step re-assembly for time-dependent coefficients (driver.cpp:37-41,
   // problem.cpp:50-71): new UNSCALED samples (device arrays) replace the
@@ -121,6 +124,7 @@ class StructuredOp {
   mutable DevBuf<double> d_q_, d_xT_;
   bool transpose_columns_ = true;
   bool host_stale_ = false;
+  mutable bool frozen_ = false;
 };
 
 }  // namespace fde_b200

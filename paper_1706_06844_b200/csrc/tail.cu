@@ -179,12 +179,12 @@ __global__ void __launch_bounds__(kTailThreads) k_vcycle_tail(const TailDesc d) 
 }  // namespace
 
 void launch_vcycle_tail(const TailDesc& d, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
+  static DeviceCache<bool> configured;  // per device
+  configured.get([](int) {
     FDE_CUDA(cudaFuncSetAttribute(k_vcycle_tail, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(kTailSmemMax * sizeof(double))));
-    configured = true;
-  }
+    return true;
+  });
   launch_k(k_vcycle_tail, 1, kTailThreads, (size_t)d.smem * sizeof(double), s, d);
   FDE_LAUNCH_CHECK();
 }

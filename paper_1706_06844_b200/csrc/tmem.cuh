@@ -52,6 +52,15 @@ __device__ __forceinline__ void tmem_st4(uint32_t taddr, const double2 (&v)[4]) 
       "r"(__double2hiint(v[3].y))
       : "memory");
 }
+// 2 complex doubles (8 columns) at column offset `taddr`
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, const double2 (&v)[2]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+      "r"(__double2loint(v[0].x)), "r"(__double2hiint(v[0].x)), "r"(__double2loint(v[0].y)),
+      "r"(__double2hiint(v[0].y)), "r"(__double2loint(v[1].x)), "r"(__double2hiint(v[1].x)),
+      "r"(__double2loint(v[1].y)), "r"(__double2hiint(v[1].y))
+      : "memory");
+}
 // load + wait in one asm statement, so no consumer can be scheduled between
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, double2 (&v)[4]) {
   int r[16];

@@ -222,6 +222,73 @@ __global__ void k_mgs(size_t n, double* __restrict__ w, const double* __restrict
   reduce_finish<1>(acc, partials, counter, outs, sq);
 }
 
+// ---- fused BiCGSTAB updates (scalars stay on the device) --------------------
+// sc[] slots: see BicgSlot (vec_kernels.cuh).  Quotients are formed on the
+// device from finished reductions, in the oracle's order of operations.
+// s = r - alpha v with alpha = rho / <rh, v>;  *ns = ||s||
+__global__ void k_bicg_s(size_t n, const double* __restrict__ r, const double* __restrict__ v,
+                         double* __restrict__ sv, double* sc, int rho_slot, double* partials,
+                         unsigned int* counter) {
+  pdl_enter();
+  const double alpha = sc[rho_slot] / sc[BICG_RV];
+  double acc[1] = {0.0};
+  GRID_STRIDE(i, n) {
+    const double si = r[i] - alpha * v[i];
+    sv[i] = si;
+    acc[0] = fma(si, si, acc[0]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc[BICG_ALPHA] = alpha;
+  double* const outs[1] = {sc + BICG_NS};
+  const int sq[1] = {1};
+  reduce_finish<1>(acc, partials, counter, outs, sq);
+}
+// tt = <t, t>, ts = <t, s> in one pass over t
+__global__ void k_bicg_tt(size_t n, const double* __restrict__ t, const double* __restrict__ sv,
+                          double* sc, double* partials, unsigned int* counter) {
+  pdl_enter();
+  double acc[2] = {0.0, 0.0};
+  GRID_STRIDE(i, n) {
+    const double ti = t[i];
+    acc[0] = fma(ti, ti, acc[0]);
+    acc[1] = fma(ti, sv[i], acc[1]);
+  }
+  double* const outs[2] = {sc + BICG_TT, sc + BICG_TS};
+  const int sq[2] = {0, 0};
+  reduce_finish<2>(acc, partials, counter, outs, sq);
+}
+// omega = ts / tt (0 when tt == 0);  x += alpha p + omega s;  r = s - omega t;
+// *nr = ||r||, sc[rho_out] = <rh, r> (the next iteration's rho)
+__global__ void k_bicg_xr(size_t n, const double* __restrict__ p, const double* __restrict__ sv,
+                          const double* __restrict__ t, const double* __restrict__ rh,
+                          double* __restrict__ x, double* __restrict__ r, double* sc, int rho_out,
+                          double* partials, unsigned int* counter) {
+  pdl_enter();
+  const double alpha = sc[BICG_ALPHA];
+  const double tt = sc[BICG_TT];
+  const double omg = tt > 0.0 ? sc[BICG_TS] / tt : 0.0;
+  double acc[2] = {0.0, 0.0};
+  GRID_STRIDE(i, n) {
+    const double si = sv[i];
+    x[i] += alpha * p[i] + omg * si;
+    const double ri = si - omg * t[i];
+    r[i] = ri;
+    acc[0] = fma(ri, ri, acc[0]);
+    acc[1] = fma(rh[i], ri, acc[1]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc[BICG_OMEGA] = omg;
+  double* const outs[2] = {sc + BICG_NR, sc + rho_out};
+  const int sq[2] = {1, 0};
+  reduce_finish<2>(acc, partials, counter, outs, sq);
+}
+// p = r + beta (p - omega v), beta = (rho_new / rho_old) (alpha / omega)
+__global__ void k_bicg_p(size_t n, const double* __restrict__ r, const double* __restrict__ v,
+                         double* __restrict__ p, const double* sc, int rho_new, int rho_old) {
+  pdl_enter();
+  const double omg = sc[BICG_OMEGA];
+  const double beta = (sc[rho_new] / sc[rho_old]) * (sc[BICG_ALPHA] / omg);
+  GRID_STRIDE(i, n) p[i] = r[i] + beta * (p[i] - omg * v[i]);
+}
+
 // ---- grid transfers ---------------------------------------------------------
 // restrict_rows (multigrid.cpp:46-58): v = f[fc]; v += .5 f[fc-1]; v += .5 f[fc+1]; scale*v
 __device__ __forceinline__ double rrow(const double* f, int n, int fc, double sc) {
@@ -540,6 +607,30 @@ void Reducer::dot(size_t n, const double* x, const double* y, double* out, cudaS
   FDE_LAUNCH_CHECK();
 }
 
+void Reducer::bicg_s(size_t n, const double* r, const double* v, double* sv, double* sc,
+                     int rho_slot, cudaStream_t s) {
+  launch_k(k_bicg_s, blocks_for(n), kThreads, 0, s, n, r, v, sv, sc, rho_slot, partials_.get(),
+           counter_.get());
+  FDE_LAUNCH_CHECK();
+}
+void Reducer::bicg_tt(size_t n, const double* t, const double* sv, double* sc, cudaStream_t s) {
+  launch_k(k_bicg_tt, blocks_for(n), kThreads, 0, s, n, t, sv, sc, partials_.get(),
+           counter_.get());
+  FDE_LAUNCH_CHECK();
+}
+void Reducer::bicg_xr(size_t n, const double* p, const double* sv, const double* t,
+                      const double* rh, double* x, double* r, double* sc, int rho_out,
+                      cudaStream_t s) {
+  launch_k(k_bicg_xr, blocks_for(n), kThreads, 0, s, n, p, sv, t, rh, x, r, sc, rho_out,
+           partials_.get(), counter_.get());
+  FDE_LAUNCH_CHECK();
+}
+void Reducer::bicg_p(size_t n, const double* r, const double* v, double* p, const double* sc,
+                     int rho_new, int rho_old, cudaStream_t s) {
+  launch_k(k_bicg_p, blocks_for(n), kThreads, 0, s, n, r, v, p, sc, rho_new, rho_old);
+  FDE_LAUNCH_CHECK();
+}
+
 void Reducer::norm_dot(size_t n, const double* w, const double* v, double* norm_out,
                        double* dot_out, cudaStream_t s) {
   launch_k(k_norm_dot, blocks_for(n), kThreads, 0, s, n, w, v, partials_.get(), counter_.get(),
@@ -548,12 +639,14 @@ void Reducer::norm_dot(size_t n, const double* w, const double* v, double* norm_
 }
 bool Reducer::mgs_chain(size_t n, double* w, const double* const* v_dev, int last, double* dh,
                         double* dnorm0, double* dnrmw, double* vout, cudaStream_t s) {
-  static int grid = -1;
-  static size_t max_smem = 0;
-  if (grid < 0) {
-    grid = 0;
-    int dev = 0, sms = 0, coop = 0, optin = 0;
-    FDE_CUDA(cudaGetDevice(&dev));
+  struct Setup {
+    int grid;
+    size_t max_smem;
+  };
+  static DeviceCache<Setup> setup;  // per device: cooperative grid, opt-in shared memory
+  const Setup& su = setup.get([](int dev) {
+    Setup r{0, 0};
+    int sms = 0, coop = 0, optin = 0;
     FDE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     FDE_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
     FDE_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -562,12 +655,15 @@ bool Reducer::mgs_chain(size_t n, double* w, const double* const* v_dev, int las
     if (coop) {
       cudaFuncAttributes fa{};
       FDE_CUDA(cudaFuncGetAttributes(&fa, k_mgs_chain));
-      max_smem = (size_t)optin - fa.sharedSizeBytes;
+      r.max_smem = (size_t)optin - fa.sharedSizeBytes;
       FDE_CUDA(cudaFuncSetAttribute(k_mgs_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)max_smem));
-      grid = sms;
+                                    (int)r.max_smem));
+      r.grid = sms;
     }
-  }
+    return r;
+  });
+  const int grid = su.grid;
+  const size_t max_smem = su.max_smem;
   if (grid == 0) return false;
   const size_t chunk = ((n + grid - 1) / grid + 1) & ~size_t(1);
   if (chunk * sizeof(double) > max_smem) return false;
@@ -661,6 +757,52 @@ void lu_solve(int n, const double* lu, const int* perm, const double* b, double*
               cudaStream_t s) {
   launch_k(k_lu_solve, 1, 256, (size_t)n * sizeof(double), s, n, lu, perm, b, x);
   FDE_LAUNCH_CHECK();
+}
+
+// ---- FP64 roofline denominator, measured where the bench runs ---------------
+// Eight independent DFMA chains per thread (inline PTX: the compiler keeps
+// every one), 8 CTAs of 256 threads per SM: saturates the FP64 pipe.
+namespace {
+__global__ void __launch_bounds__(256) k_dfma_probe(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-9 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[i]) : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+}  // namespace
+
+double fp64_peak_tflops(cudaStream_t s) {
+  int dev = current_device(), sms = 0;
+  FDE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int blocks = sms * 8, threads = 256, iters = 2048;
+  DevBuf<double> out((size_t)blocks * threads);
+  cudaEvent_t e0, e1;
+  FDE_CUDA(cudaEventCreate(&e0));
+  FDE_CUDA(cudaEventCreate(&e1));
+  double best = 0.0;
+  for (int rep = 0; rep < 4; ++rep) {  // first repetition warms up
+    FDE_CUDA(cudaEventRecord(e0, s));
+    k_dfma_probe<<<blocks, threads, 0, s>>>(out.get(), iters, 0.999999, 1e-7);
+    FDE_LAUNCH_CHECK();
+    FDE_CUDA(cudaEventRecord(e1, s));
+    FDE_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    FDE_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    const double tf = 2.0 * 8 * 16 * (double)iters * blocks * threads / (ms * 1e9);
+    if (rep > 0 && tf > best) best = tf;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return best;
 }
 
 }  // namespace fde_b200

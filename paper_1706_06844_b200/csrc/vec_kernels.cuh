@@ -32,6 +32,22 @@ void vec_sub(size_t n, const double* x, const double* y, double* out, cudaStream
 void vec_lincomb(size_t n, const double* x0, const double* const* v_dev, const double* c_dev,
                  int k, double* out, cudaStream_t s);
 
+// Device scalar slots of the fused BiCGSTAB iteration (krylov.cu): reductions
+// land here, the quotients alpha, omega, beta are formed on the device, and
+// the host reads the block back twice per iteration for its control flow.
+enum BicgSlot : int {
+  BICG_RHO_A = 0,  // <rh, r>, alternating with BICG_RHO_B between iterations
+  BICG_RHO_B = 1,
+  BICG_RV = 2,     // <rh, v>
+  BICG_ALPHA = 3,
+  BICG_NS = 4,     // ||s||
+  BICG_TT = 5,     // <t, t>
+  BICG_TS = 6,     // <t, s>
+  BICG_OMEGA = 7,
+  BICG_NR = 8,     // ||r||
+  BICG_SLOTS = 9
+};
+
 // Deterministic two-level dot product: per-block partials + last-block sum in
 // fixed order.  Writes <x,y> to *out_dev (and sqrt to *out_dev if sqrt_out).
 class Reducer {
@@ -42,6 +58,19 @@ class Reducer {
   // *norm_out = ||w||, *dot_out = <v, w> in one pass (first MGS projection)
   void norm_dot(size_t n, const double* w, const double* v, double* norm_out, double* dot_out,
                 cudaStream_t s);
+  // Fused BiCGSTAB passes on the device scalar block sc[BICG_SLOTS]:
+  //   bicg_s : alpha = sc[rho_slot] / sc[RV]; s = r - alpha v; sc[NS] = ||s||
+  //   bicg_tt: sc[TT] = <t,t>, sc[TS] = <t,s>
+  //   bicg_xr: omega = TS/TT; x += alpha p + omega s; r = s - omega t;
+  //            sc[NR] = ||r||, sc[rho_out] = <rh, r>
+  //   bicg_p : p = r + beta (p - omega v), beta = (rho_new/rho_old)(alpha/omega)
+  void bicg_s(size_t n, const double* r, const double* v, double* sv, double* sc, int rho_slot,
+              cudaStream_t s);
+  void bicg_tt(size_t n, const double* t, const double* sv, double* sc, cudaStream_t s);
+  void bicg_xr(size_t n, const double* p, const double* sv, const double* t, const double* rh,
+               double* x, double* r, double* sc, int rho_out, cudaStream_t s);
+  void bicg_p(size_t n, const double* r, const double* v, double* p, const double* sc,
+              int rho_new, int rho_old, cudaStream_t s);
   // w -= (*hk) v_k, then *out = <v_next, w> (sqrt when sqrt_out; v_next may be w)
   void mgs(size_t n, double* w, const double* vk, const double* hk, const double* vnext,
            double* out, bool sqrt_out, cudaStream_t s);
@@ -89,5 +118,10 @@ void block_permute(const double* in, double* out, size_t nc, size_t d2, const lo
 // x = U^-1 L^-1 P b on one CTA (coarsest CoarseSolve::lu, multigrid.cpp:324-328).
 void lu_solve(int n, const double* lu, const int* perm, const double* b, double* x,
               cudaStream_t s);
+
+// Measured DFMA throughput of the current device in TFLOP/s (best of three
+// timed launches of a pure FP64 FMA kernel): the roofline denominator of the
+// FP64-issue-bound line kernels, taken in the run that reports the fraction.
+double fp64_peak_tflops(cudaStream_t s);
 
 }  // namespace fde_b200

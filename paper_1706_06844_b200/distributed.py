@@ -566,6 +566,12 @@ class DistMarch:
                  omega=0.7, coarse=COARSE_SWEEPS, coarse_sweeps=3, agglomerate=65536, precond=True,
                  ratio0=None):
         self.ctx, self.bk = ctx, ctx.backend
+        if getattr(problem, "time_dependent_coeffs", False):
+            # the operator and the hierarchy are built once (at m = 1): a
+            # time-dependent problem needs the t^{m-1} operator for the rhs and
+            # the step-m operator and V-cycle for the solve (driver.cpp:37-51)
+            raise NotImplementedError("the y-slab march supports time-independent coefficients "
+                                      "only; use the single-GPU March for time-dependent problems")
         self.problem, self.n1, self.n2, self.steps = problem, n1, n2, steps
         self.tol, self.restart, self.max_outer = tol, restart, max_outer
         rows = split_ranges(n2, ctx.world)

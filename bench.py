@@ -70,7 +70,48 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-FP64_PEAK_TFLOPS = 34.19  # profiles/fp64_peak_r01.txt: DFMA loop on this pool's B200
+FP64_PEAK_FALLBACK = 34.19  # profiles/fp64_peak_r01.txt (used only if the in-run probe fails)
+
+
+def fp64_peak_in_run(fde):
+    """FP64 roofline denominator measured in this run: the library's DFMA loop
+    (fde_fp64_peak, csrc/vec_kernels.cu) on the bench's own device and clocks."""
+    try:
+        v = max(fde.fp64_peak_tflops() for _ in range(3))
+        return float(v), "measured in this run: fde_fp64_peak DFMA loop (best of 3)"
+    except Exception as e:  # pragma: no cover - library too old
+        return FP64_PEAK_FALLBACK, f"fallback profiles/fp64_peak_r01.txt ({e})"
+
+
+def dram_traffic_in_run(local: int):
+    """DRAM bytes of one n=2047 operator apply, every kernel of the apply
+    counted (transpose, column pass, row pass) plus the write-back of the dirty
+    lines it leaves in L2: tools/traffic_probe.py run under a metrics-only ncu
+    pass in a subprocess, after the timed legs.  None when ncu cannot profile
+    on this box (the reason is logged)."""
+    import shutil
+    import tempfile
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not Path(ncu).exists():
+        return None, "ncu not found"
+    with tempfile.TemporaryDirectory() as td:
+        csvf = Path(td) / "traffic.csv"
+        env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", str(local)))
+        for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+            env.pop(k, None)
+        cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control",
+               "none", "-k", "regex:line_kernel|transpose|FillFunctor", "--csv", "--log-file",
+               str(csvf), sys.executable, str(ROOT / "tools" / "traffic_probe.py"), str(N), "3"]
+        try:
+            r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=240)
+            if r.returncode != 0 or not csvf.exists():
+                return None, f"ncu rc={r.returncode}: {(r.stderr or r.stdout)[-200:]}"
+            sys.path.insert(0, str(ROOT / "tools"))
+            import traffic_probe
+            d = traffic_probe.parse(csvf)
+            return d, "ok"
+        except Exception as e:
+            return None, f"{type(e).__name__}: {e}"
 
 
 def apply_flops(n1: int, n2: int) -> float:
@@ -201,6 +242,86 @@ def cpu_baseline_sample(iters_per_step: float):
             "apply_seconds": ta, "vcycle_seconds": tv}
 
 
+def other_configs(fde, torch, dev, stream, hbm_peak):
+    """The other BASELINE configs, reported beside the headline: cfg1-3 marches
+    (steps/s of a second, warm march; GMRES / BiCGSTAB iteration totals) and
+    the five cfg5 rows (apply and V-cycle GB/s and HBM fraction, L2 flushed)."""
+    out = {}
+
+    def march_rate(k, n, steps, **kw):
+        cfg = fde.DriverConfig(precond=fde.PRECOND_MGM, tol=kw.get("tol", 1e-8),
+                               restart=kw.get("restart", 20), max_outer=100, omega=0.7, cycles=1,
+                               coarse=kw.get("coarse", fde.COARSE_SWEEPS), coarse_sweeps=3,
+                               solver=kw.get("solver", 0))
+        prob = fde.Problem.preset_config(k, seed=0)
+        rate, its = None, None
+        for rep_ in range(2):  # the second march is timed (graphs captured, caches warm)
+            march = fde.March(prob, n, n, steps, cfg)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            its = [march.step()[0] for _ in range(steps)]
+            b.record(stream)
+            b.synchronize()
+            rate = steps / (a.elapsed_time(b) / 1e3)
+            del march
+        return {"n": n, "steps": steps, "steps_per_s": rate, "iterations": int(sum(its))}
+
+    try:
+        out["cfg1"] = dict(march_rate(1, 63, 64), solver="gmres(20)+mgm")
+        out["cfg2"] = dict(march_rate(2, 255, 32), solver="gmres(20)+mgm")
+        for name, kw in (("cfg3_gmres30_vcycle_lu", dict(coarse=fde.COARSE_LU)),
+                         ("cfg3_gmres30_geometric_sweeps", dict(coarse=fde.COARSE_SWEEPS)),
+                         ("cfg3_bicgstab_vcycle_lu", dict(coarse=fde.COARSE_LU, solver=1)),
+                         ("cfg3_bicgstab_geometric_sweeps", dict(coarse=fde.COARSE_SWEEPS, solver=1))):
+            out[name] = dict(march_rate(3, 1023, 16, tol=1e-10, restart=30, **kw),
+                             solver=name.split("_", 1)[1])
+    except Exception as e:
+        out["march_error"] = f"{type(e).__name__}: {e}"
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=dev)
+
+    def timed(fn, reps=7):
+        ts = []
+        for r in range(reps + 2):
+            flush.fill_(float(r))
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            if r >= 2:
+                ts.append(a.elapsed_time(b) / 1e3)
+        return statistics.median(ts)
+
+    rows = []
+    try:
+        for n in (511, 1023, 2047, 4095, 8191):
+            p = fde.Problem.preset_config(5, steps=1)
+            op = fde.StructuredFdeOperator.assemble(p, n, n, 1, 1)
+            g = torch.Generator(device=dev).manual_seed(n)
+            x = torch.rand(n * n, dtype=torch.float64, device=dev, generator=g) * 2 - 1
+            y = torch.empty_like(x)
+            t_a = timed(lambda: op.apply(x, y))
+            h = fde.MgHierarchy.build_geometric(p, n, n, 1, 1, 0.7, fde.COARSE_SWEEPS, 3)
+            nl = [a * b for a, b in h.dims()]
+            z = torch.zeros_like(x)
+            t_v = timed(lambda: h.vcycle(x, z, zero_guess=True))
+            b_v = sum(168 * nl[l] + 16 * nl[l + 1] for l in range(len(nl) - 1)) + 152 * nl[-1]
+            b_a = 48 * n * n
+            rows.append({"n": n, "apply_us": t_a * 1e6, "apply_GBps": b_a / t_a / 1e9,
+                         "apply_frac_hbm": b_a / t_a / 1e9 / hbm_peak,
+                         "vcycle_us": t_v * 1e6, "vcycle_GBps": b_v / t_v / 1e9,
+                         "vcycle_frac_hbm": b_v / t_v / 1e9 / hbm_peak, "levels": len(nl)})
+            del op, h, x, y, z
+            torch.cuda.empty_cache()
+    except Exception as e:
+        out["cfg5_error"] = f"{type(e).__name__}: {e}"
+    out["cfg5"] = {"rows": rows, "bytes": "apply 48 N; V-cycle sum_l 168 N_l + 16 N_(l+1), "
+                                          "152 N_last (SURVEY 8(d)); L2 flushed, median of 7"}
+    return out
+
+
 # ---------------------------------------------------------------- own arm
 def run_own(args):
     import torch
@@ -215,7 +336,7 @@ def run_own(args):
     fde.load_library()
     stream = torch.cuda.current_stream()
     total = args.warmup + args.steps
-    prob = fde.Problem.preset_config(CFG, seed=rank, steps=total, tau=TAU)
+    prob = fde.Problem.preset_config(CFG, seed=0, steps=total, tau=TAU)  # one problem on every rank
     cfg = fde.DriverConfig(precond=fde.PRECOND_MGM, tol=1e-8, restart=20, max_outer=100,
                            omega=0.7, cycles=1, coarse=fde.COARSE_SWEEPS, coarse_sweeps=3)
 
@@ -330,10 +451,14 @@ def run_own(args):
     achieved = bytes_apply / t_apply / 1e9
     flops = apply_flops(N, N)
     fp64 = flops / t_apply / 1e12
-    traffic = None
-    tp = ROOT / "profiles" / "apply_traffic.json"
-    if tp.exists():
-        traffic = json.loads(tp.read_text()).get("bytes_per_apply")
+    fp64_peak, fp64_src = fp64_peak_in_run(fde)
+    del op, x, y, flush
+    torch.cuda.empty_cache()
+    other = None if args.no_other_configs else other_configs(fde, torch, dev, stream, hbm_peak)
+    torch.cuda.empty_cache()
+    td, tmsg = (None, "skipped (--no-traffic)") if args.no_traffic else dram_traffic_in_run(local)
+    traffic = td["bytes_per_apply"] if td else None
+    log(f"[bench] traffic probe: {tmsg}")
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -351,13 +476,18 @@ def run_own(args):
                            "algorithmic_flops": flops},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
+                     "traffic_source": ("in-run ncu pass over tools/traffic_probe.py: every kernel "
+                                        "of the apply + the write-back of its dirty L2 lines"
+                                        if td else f"null: {tmsg}"),
+                     "traffic_over_algorithmic": (traffic / bytes_apply if traffic else None),
                      "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs (burst copy)",
                      "kernel": "operator apply = y-pass + x-pass line-FFT kernels (48 B/unknown)",
-                     "fp64": {"achieved": fp64, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                              "frac": fp64 / FP64_PEAK_TFLOPS,
-                              "peak_source": "measured DFMA loop, profiles/fp64_peak_r01.txt"}},
+                     "fp64": {"achieved": fp64, "peak": fp64_peak, "unit": "TFLOP/s",
+                              "frac": fp64 / fp64_peak, "peak_source": fp64_src}},
         "clocks": clocks,
     }
+    if other:
+        out["configs"] = other
     if rank == 0 and not args.no_cpu_baseline:
         try:
             k = float(np.mean(timed_its)) if timed_its else 12.0
@@ -373,20 +503,19 @@ def run_own(args):
 
 
 def run_own_distributed(args, prob, cfg, rank, world, local, dev, stream, barrier):
-    """N > 1: y-slab decomposition (paper_1706_06844_b200.distributed) over NCCL;
-    every rank owns n/N grid rows; steps/s of the whole job (max over ranks)."""
+    """N > 1: y-slab decomposition, C++ host over NCCL (csrc/dist.cu, fde.SlabMarch);
+    every rank owns n/N grid rows of the SAME cfg4 problem (seed 0), so the job
+    is the N = 1 job split N ways (strong scaling); steps/s of the whole job,
+    device-timed, max over ranks."""
     import torch
     import paper_1706_06844_b200 as fde
-    from paper_1706_06844_b200 import distributed as D
 
     total = args.warmup + args.steps
-    ctx = D.DistContext(rank, world, D.GpuBackend(dev))
-    march = D.DistMarch(ctx, prob, N, N, total, tol=cfg.tol, restart=cfg.restart,
-                        max_outer=cfg.max_outer, omega=cfg.omega, coarse=cfg.coarse,
-                        coarse_sweeps=cfg.coarse_sweeps)
-    lv = march.level
-    srcs = [torch.tensor(prob.sample_source(N, N, total, m)[lv.r0 * N:lv.r1 * N], device=dev)
-            for m in range(1, total + 1)]
+    march = fde.SlabMarch(prob, N, N, total, cfg, rank=rank, world=world)
+    nloc = march.local_size
+    rows = slice(march.r0 * N, march.r1 * N)
+    host_src = [prob.sample_source(N, N, total, m)[rows] for m in range(1, total + 1)]
+    srcs = [torch.tensor(h, device=dev) for h in host_src]
     its = [march.step(srcs[m])[0] for m in range(args.warmup)]
     barrier()
     clk = ClockSampler(local)
@@ -402,20 +531,92 @@ def run_own_distributed(args, prob, cfg, rank, world, local, dev, stream, barrie
     barrier()
     clk.window(t_start, time.time())
     clocks = clk.stop()
-    ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
-    torch.distributed.all_reduce(ms, op=torch.distributed.ReduceOp.MAX)
-    ms = float(ms.item())
+    launches = fde.kernel_launches() - launches0
+
+    def max_over_ranks(v):
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = max_over_ranks(e0.elapsed_time(e1))
+
+    # e2e: every step copies this rank's source rows H2D from pinned memory and
+    # its rows of u^m back D2H, inside the timed region
+    pin_src = [torch.from_numpy(np.ascontiguousarray(h)).pin_memory() for h in host_src]
+    pin_out = torch.empty(nloc, dtype=torch.float64).pin_memory()
+    dsrc = torch.empty(nloc, dtype=torch.float64, device=dev)
+    collectives = march.collectives()
+    del march
+    torch.cuda.empty_cache()
+    march2 = fde.SlabMarch(prob, N, N, total, cfg, rank=rank, world=world)
+    dout = torch.empty(nloc, dtype=torch.float64, device=dev)
+    for m in range(args.warmup):
+        dsrc.copy_(pin_src[m], non_blocking=True)
+        march2.step(dsrc)
+    barrier()
+    e0.record(stream)
+    for m in range(args.warmup, total):
+        dsrc.copy_(pin_src[m], non_blocking=True)
+        march2.step(dsrc)
+        march2.solution_to(dout)
+        pin_out.copy_(dout, non_blocking=True)
+    e1.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+
+    # roofline: the distributed fine-level apply (transposes + both all-to-alls
+    # + both passes), L2 flushed, max over ranks; bytes = the whole grid's 48 N
+    x = torch.rand(nloc, dtype=torch.float64, device=dev) * 2 - 1
+    y = torch.empty_like(x)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=dev)
+    ts = []
+    for r in range(3 + 10):
+        flush.fill_(float(r))
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        march2.apply(x, y)
+        a1.record(stream)
+        a1.synchronize()
+        if r >= 3:
+            ts.append(max_over_ranks(a0.elapsed_time(a1)) / 1e3)
+    t_apply = float(np.mean(ts))
+    hbm_peak, peak_kind = measured_peaks()
+    bytes_apply = 48.0 * N * N
+    achieved = bytes_apply / t_apply / 1e9
+    fp64_peak, fp64_src = fp64_peak_in_run(fde)
+    fp64 = apply_flops(N, N) / t_apply / 1e12
     out = {
         "metric": METRIC, "value": args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded counter-hash U[0,1) source, SURVEY Appendix A)",
-        "config": dict(CONFIG, parallelism=f"y-slab x{world} (NCCL all-to-all transposes, "
-                                         f"ordered all-gather dots, replicated coarse tail)"),
+        "config": dict(CONFIG, parallelism=f"y-slab x{world} (C++ host, NCCL send/recv all-to-all "
+                                         f"transposes, rank-ordered all-gather dots, replicated "
+                                         f"coarse tail, graph-captured V-cycle)"),
         "iterations_per_step": [int(v) for v in timed], "warmup_iterations": [int(v) for v in its],
-        "gpu_launches": int(fde.kernel_launches() - launches0), "clocks": clocks,
-        "e2e": None,
+        "gpu_launches": int(launches), "clocks": clocks,
+        "collectives_per_step": collectives / max(total, 1),
+        "e2e": {"value": args.steps / (e2e_ms / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": 8 * N * N, "d2h_bytes_per_step": 8 * N * N,
+                "note": "whole-job bytes; each rank copies its own rows"},
+        "operator_apply": {"seconds": t_apply, "GB_per_s": achieved, "algorithmic_bytes": bytes_apply,
+                           "fp64_TFLOP_per_s": fp64},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak * world, "unit": "GB/s",
+                     "frac": achieved / (hbm_peak * world), "traffic": None,
+                     "peak_source": f"{world} x {peak_kind} MEASURED_PEAKS.json hbm_gbs",
+                     "kernel": "distributed operator apply: local transposes, two NCCL all-to-alls, "
+                               "column pass on owned columns, row pass on owned rows",
+                     "fp64": {"achieved": fp64, "peak": fp64_peak * world, "unit": "TFLOP/s",
+                              "frac": fp64 / (fp64_peak * world), "peak_source": fp64_src}},
     }
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            out["cpu_baseline"] = cpu_baseline_sample(float(np.mean(timed)) if timed else 12.0)
+        except Exception as e:
+            out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                                   "sample": f"unavailable: {e}"}
+    barrier()
     if rank == 0:
         print(json.dumps(out), flush=True)
     torch.distributed.destroy_process_group()
@@ -429,6 +630,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the in-run ncu traffic probe")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the cfg1-3 marches and the cfg5 sweep")
     ap.add_argument("--steps-only", action="store_true",
                     help="time the steps only (for launch-list profiling)")
     args = ap.parse_args()

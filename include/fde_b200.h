@@ -300,6 +300,49 @@ int fde_dot(size_t n, const double* x, const double* y, double* out_dev, int sqr
 
 /* Number of kernels this library has launched since load (instrumentation). */
 unsigned long long fde_kernel_launches(void);
+/* ------------------------------------------------ multi-GPU time step
+ * The per-step loop of the y-slab decomposition in C++ (csrc/dist.cu): slab
+ * levels, the distributed V-cycle with its replicated coarse tail, GMRES with
+ * device-resident scalars and rank-ordered inner products, and the march
+ * (reference: driver.cpp:10-69, krylov.cpp:34-166, multigrid.cpp:318-394 --
+ * the reference itself is single-process).  One process per GPU; the
+ * transport is NCCL, opened at run time.  fde_dist_unique_id on one rank
+ * produces the 128-byte id every rank passes to fde_dist_comm_create (the
+ * launcher moves it, e.g. by a torch.distributed broadcast). */
+typedef struct fde_dist_comm_s* fde_dist_comm;
+int fde_dist_unique_id(unsigned char* id128);
+int fde_dist_comm_create(const unsigned char* id128, int rank, int world, fde_dist_comm* out);
+int fde_dist_comm_destroy(fde_dist_comm c);
+typedef struct fde_dist_march_s* fde_dist_march;
+/* cfg: solver 0 (gmres), precond none or mgm, cycles 1.  Levels of at most
+ * `agglomerate` unknowns are replicated on every rank. */
+int fde_dist_march_create(fde_dist_comm c, const fde_problem* p, size_t n1, size_t n2,
+                          size_t steps, const fde_driver_config* cfg, size_t agglomerate,
+                          fde_dist_march* out);
+/* grid rows [r0, r1) this rank owns; local vectors hold (r1 - r0) * n1 values */
+int fde_dist_march_rows(fde_dist_march h, size_t* r0, size_t* r1);
+/* one time step; source_local: the rank's rows of v(., t^{m-1/2}) on the
+ * DEVICE, or NULL (evaluated by the library) */
+int fde_dist_march_step(fde_dist_march h, const double* source_local, void* stream,
+                        size_t* iterations, double* residual);
+int fde_dist_march_solution(fde_dist_march h, double* u_local, int to_host, void* stream);
+int fde_dist_march_solution_ptr(fde_dist_march h, const double** u_dev);
+/* y_local = (A x)_local and x_local = V-cycle(b_local): device arrays */
+int fde_dist_march_apply(fde_dist_march h, const double* x_local, double* y_local, void* stream);
+int fde_dist_march_vcycle(fde_dist_march h, const double* b_local, double* x_local, void* stream);
+/* collectives issued so far (all-to-all, all-gather, halo exchanges) */
+int fde_dist_march_collectives(fde_dist_march h, unsigned long long* n);
+int fde_dist_march_destroy(fde_dist_march h);
+/* The same code on `nranks` VIRTUAL ranks of the current device (one host
+ * thread per rank, one shared stream, collectives as ordered device copies):
+ * how the N > 1 paths are exercised on one GPU.  HOST vectors of the whole
+ * grid.  what 0: march `nrun` steps, out = u^nrun, iterations / residuals
+ * [nrun]; what 1: out = A in; what 2: out = V-cycle(in). */
+int fde_vdist_run(const fde_problem* p, size_t n1, size_t n2, size_t steps,
+                  const fde_driver_config* cfg, int nranks, size_t agglomerate, int what,
+                  size_t nrun, const double* in_full, double* out_full, size_t* iterations,
+                  double* residuals, unsigned long long* collectives);
+
 /* Measured FP64 FMA throughput of the current device in TFLOP/s (a pure DFMA
  * kernel, best of three timed launches): the roofline denominator of the
  * FP64-issue-bound line kernels, taken in the reporting run. */

@@ -28,7 +28,7 @@ __all__ = [
     "load_library", "library_path", "wsgd_weights", "binom_coeffs", "Problem",
     "StructuredFdeOperator", "MgHierarchy", "Preconditioner", "make_preconditioner",
     "SolverConfig", "KrylovResult", "gmres", "bicgstab", "DriverConfig", "March",
-    "SolveReport", "time_march", "plan_level_dims", "transfer", "kernel_launches",
+    "SolveReport", "time_march", "SlabMarch", "vdist_run", "plan_level_dims", "transfer", "kernel_launches",
     "PRECOND_NONE", "PRECOND_P2", "PRECOND_MGM", "PRECOND_P2_EXACT", "PRECOND_MGM_GALERKIN",
     "COARSE_LU", "COARSE_SWEEPS", "COARSE_NONE",
 ]
@@ -154,6 +154,23 @@ _SIGS = {
                                    _c_int, _c_int, _c_vp]),
     "fde_axpy_dev": (_c_int, [_c_size, _c_vp, _c_dbl, _c_vp, _c_vp, _c_vp]),
     "fde_dot": (_c_int, [_c_size, _c_vp, _c_vp, _c_vp, _c_int, _c_vp]),
+    "fde_dist_unique_id": (_c_int, [ctypes.c_char_p]),
+    "fde_dist_comm_create": (_c_int, [ctypes.c_char_p, _c_int, _c_int, ctypes.POINTER(_c_vp)]),
+    "fde_dist_comm_destroy": (_c_int, [_c_vp]),
+    "fde_dist_march_create": (_c_int, [_c_vp, ctypes.POINTER(_FdeProblem), _c_size, _c_size, _c_size,
+                                       ctypes.POINTER(_DriverConfig), _c_size, ctypes.POINTER(_c_vp)]),
+    "fde_dist_march_rows": (_c_int, [_c_vp, ctypes.POINTER(_c_size), ctypes.POINTER(_c_size)]),
+    "fde_dist_march_step": (_c_int, [_c_vp, _c_vp, _c_vp, ctypes.POINTER(_c_size), _P]),
+    "fde_dist_march_solution": (_c_int, [_c_vp, _c_vp, _c_int, _c_vp]),
+    "fde_dist_march_solution_ptr": (_c_int, [_c_vp, ctypes.POINTER(_c_vp)]),
+    "fde_dist_march_apply": (_c_int, [_c_vp, _c_vp, _c_vp, _c_vp]),
+    "fde_dist_march_vcycle": (_c_int, [_c_vp, _c_vp, _c_vp, _c_vp]),
+    "fde_dist_march_collectives": (_c_int, [_c_vp, ctypes.POINTER(ctypes.c_ulonglong)]),
+    "fde_dist_march_destroy": (_c_int, [_c_vp]),
+    "fde_vdist_run": (_c_int, [ctypes.POINTER(_FdeProblem), _c_size, _c_size, _c_size,
+                               ctypes.POINTER(_DriverConfig), _c_int, _c_size, _c_int, _c_size,
+                               _c_vp, _c_vp, ctypes.POINTER(_c_size), _c_vp,
+                               ctypes.POINTER(ctypes.c_ulonglong)]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGS)
 
@@ -676,3 +693,99 @@ def time_march(problem: Problem, n1: int, n2: int, steps: int, cfg: DriverConfig
         rep.has_error = True
         rep.error_inf = problem.error_inf(u, n1, n2, steps, problem.t_final)
     return rep
+
+
+# ------------------------------------------------------------------ multi-GPU
+class SlabMarch:
+    """time_march on y-slabs, one process per GPU (csrc/dist.cu over NCCL): this
+    rank's rows [r0, r1) of u^m stay on its device.  The NCCL id is made on
+    rank 0 and moved by torch.distributed (any backend) when world > 1."""
+
+    def __init__(self, problem: Problem, n1: int, n2: int, steps: int, cfg: DriverConfig,
+                 rank: int = 0, world: int = 1, agglomerate: int = 65536):
+        lib = load_library()
+        idbuf = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _check(lib.fde_dist_unique_id(idbuf))
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            t = torch.frombuffer(bytearray(idbuf.raw), dtype=torch.uint8).clone()
+            if dist.get_backend() == "nccl":
+                t = t.cuda()
+            dist.broadcast(t, src=0)
+            idbuf = ctypes.create_string_buffer(bytes(t.cpu().numpy().tobytes()), 128)
+        self._comm = _c_vp()
+        _check(lib.fde_dist_comm_create(idbuf, rank, world, ctypes.byref(self._comm)))
+        self._s, self._cfg = problem.c_struct(), cfg.c_struct()
+        self._h = _c_vp()
+        _check(lib.fde_dist_march_create(self._comm, ctypes.byref(self._s), n1, n2, steps,
+                                         ctypes.byref(self._cfg), agglomerate, ctypes.byref(self._h)))
+        r0, r1 = _c_size(), _c_size()
+        _check(lib.fde_dist_march_rows(self._h, ctypes.byref(r0), ctypes.byref(r1)))
+        self.n1, self.n2, self.r0, self.r1 = n1, n2, r0.value, r1.value
+        self.local_size = (self.r1 - self.r0) * n1
+
+    def step(self, source_local=None, stream=None):
+        """source_local: CUDA tensor with this rank's rows of the source, or None."""
+        it, res = _c_size(), _c_dbl()
+        ptr = None if source_local is None else _dev_ptr(source_local)
+        _check(load_library().fde_dist_march_step(self._h, ptr, _stream(stream), ctypes.byref(it),
+                                                  ctypes.byref(res)))
+        return it.value, res.value
+
+    def solution_local(self) -> np.ndarray:
+        out = np.zeros(self.local_size)
+        _check(load_library().fde_dist_march_solution(self._h, out.ctypes.data, 1, _stream()))
+        return out
+
+    def solution_to(self, tensor, stream=None) -> None:
+        """Copy this rank's rows of u^m into a CUDA tensor (stream ordered)."""
+        _check(load_library().fde_dist_march_solution(self._h, _dev_ptr(tensor), 0, _stream(stream)))
+
+    def apply(self, x_local, y_local, stream=None) -> None:
+        _check(load_library().fde_dist_march_apply(self._h, _dev_ptr(x_local), _dev_ptr(y_local),
+                                                   _stream(stream)))
+
+    def vcycle(self, b_local, x_local, stream=None) -> None:
+        _check(load_library().fde_dist_march_vcycle(self._h, _dev_ptr(b_local), _dev_ptr(x_local),
+                                                    _stream(stream)))
+
+    def collectives(self) -> int:
+        n = ctypes.c_ulonglong()
+        _check(load_library().fde_dist_march_collectives(self._h, ctypes.byref(n)))
+        return int(n.value)
+
+    def __del__(self):
+        if _lib is not None:
+            if getattr(self, "_h", None):
+                _lib.fde_dist_march_destroy(self._h)
+                self._h = None
+            if getattr(self, "_comm", None):
+                _lib.fde_dist_comm_destroy(self._comm)
+                self._comm = None
+
+
+def vdist_run(problem: Problem, n1: int, n2: int, steps: int, cfg: DriverConfig, nranks: int,
+              what: str = "march", nrun: int = 1, inp: np.ndarray | None = None,
+              agglomerate: int = 65536):
+    """The multi-GPU code path on `nranks` virtual ranks of the current device.
+    what: "march" -> (u^nrun, iterations, residuals, collectives);
+    "apply" / "vcycle" -> the full-grid result vector (host arrays)."""
+    code = {"march": 0, "apply": 1, "vcycle": 2}[what]
+    out = np.zeros(n1 * n2)
+    its = (_c_size * max(nrun, 1))()
+    res = np.zeros(max(nrun, 1))
+    ncoll = ctypes.c_ulonglong()
+    s, c = problem.c_struct(), cfg.c_struct()
+    src = None
+    if code:
+        src = np.ascontiguousarray(inp, dtype=np.float64)
+        assert src.size == n1 * n2
+    _check(load_library().fde_vdist_run(ctypes.byref(s), n1, n2, steps, ctypes.byref(c), nranks,
+                                        agglomerate, code, nrun,
+                                        src.ctypes.data if src is not None else None,
+                                        out.ctypes.data, its, res.ctypes.data, ctypes.byref(ncoll)))
+    if code:
+        return out
+    return out, [int(v) for v in its][:nrun], res[:nrun].tolist(), int(ncoll.value)

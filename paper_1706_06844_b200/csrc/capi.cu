@@ -9,6 +9,8 @@
 #include "krylov.cuh"
 #include "problem.cuh"
 #include "slab.cuh"
+#include "dist.cuh"
+#include <thread>
 
 namespace fde_b200 {
 std::atomic<unsigned long long> g_kernel_launches{0};
@@ -35,6 +37,13 @@ struct fde_precond_s {
 };
 struct fde_slab_s {
   std::unique_ptr<SlabOp> op;
+};
+struct fde_dist_comm_s {
+  std::shared_ptr<SlabComm> c;
+};
+struct fde_dist_march_s {
+  std::unique_ptr<DistMarch> m;
+  DevBuf<double> tmp;
 };
 struct fde_march_s {
   Problem p;
@@ -874,6 +883,169 @@ int fde_dot(size_t n, const double* x, const double* y, double* out_dev, int sqr
     static thread_local std::unique_ptr<Reducer> red;
     if (!red) red = std::make_unique<Reducer>();
     red->dot(n, x, y, out_dev, stream_of(stream), sqrt_out != 0);
+  });
+}
+
+
+/* ------------------------------------------------ multi-GPU step (dist.cuh) */
+int fde_dist_unique_id(unsigned char* id128) {
+  return guard([&] {
+    need(id128 != nullptr, "null id");
+    nccl_unique_id(id128);
+  });
+}
+int fde_dist_comm_create(const unsigned char* id128, int rank, int world, fde_dist_comm* out) {
+  return guard([&] {
+    need(id128 && out, "null argument");
+    auto h = std::make_unique<fde_dist_comm_s>();
+    h->c = make_nccl_comm(id128, rank, world);
+    *out = h.release();
+  });
+}
+int fde_dist_comm_destroy(fde_dist_comm c) {
+  delete c;
+  return FDE_OK;
+}
+static SolverConfig solver_cfg_of(const fde_driver_config* cfg) {
+  SolverConfig sc;
+  sc.tol = cfg->tol;
+  sc.restart = cfg->restart;
+  sc.max_outer = cfg->max_outer;
+  return sc;
+}
+int fde_dist_march_create(fde_dist_comm c, const fde_problem* p, size_t n1, size_t n2,
+                          size_t steps, const fde_driver_config* cfg, size_t agglomerate,
+                          fde_dist_march* out) {
+  return guard([&] {
+    need(c && cfg && out, "null argument");
+    need(cfg->solver == 0, "the y-slab march runs GMRES");
+    need(cfg->precond == PC_NONE || cfg->precond == PC_MGM, "the y-slab march offers none / mgm");
+    need(cfg->cycles == 1 || cfg->precond == PC_NONE, "the y-slab V-cycle runs one cycle");
+    auto h = std::make_unique<fde_dist_march_s>();
+    h->m = std::make_unique<DistMarch>(c->c, to_problem(p), n1, n2, steps, solver_cfg_of(cfg),
+                                       cfg->omega, cfg->coarse, cfg->coarse_sweeps, agglomerate,
+                                       cfg->precond == PC_MGM);
+    *out = h.release();
+  });
+}
+int fde_dist_march_rows(fde_dist_march h, size_t* r0, size_t* r1) {
+  return guard([&] {
+    need(h && r0 && r1, "null argument");
+    *r0 = h->m->r0();
+    *r1 = h->m->r1();
+  });
+}
+int fde_dist_march_step(fde_dist_march h, const double* source_local, void* stream,
+                        size_t* iterations, double* residual) {
+  return guard([&] {
+    need(h != nullptr, "null march");
+    const DistReport r = h->m->step(source_local, stream_of(stream));
+    if (iterations) *iterations = r.iterations;
+    if (residual) *residual = r.final_rel;
+  });
+}
+int fde_dist_march_solution(fde_dist_march h, double* u_local, int to_host, void* stream) {
+  return guard([&] {
+    need(h && u_local, "null argument");
+    cudaStream_t s = stream_of(stream);
+    FDE_CUDA(cudaMemcpyAsync(u_local, h->m->solution(), h->m->local_size() * sizeof(double),
+                             to_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+    if (to_host) FDE_CUDA(cudaStreamSynchronize(s));
+  });
+}
+int fde_dist_march_solution_ptr(fde_dist_march h, const double** u_dev) {
+  return guard([&] {
+    need(h && u_dev, "null argument");
+    *u_dev = h->m->solution();
+  });
+}
+int fde_dist_march_apply(fde_dist_march h, const double* x_local, double* y_local, void* stream) {
+  return guard([&] {
+    need(h && x_local && y_local && x_local != y_local, "apply needs distinct buffers");
+    h->m->level().run(x_local, y_local, 1.0, EPI_STORE, EpiArgs{}, stream_of(stream));
+  });
+}
+int fde_dist_march_vcycle(fde_dist_march h, const double* b_local, double* x_local, void* stream) {
+  return guard([&] {
+    need(h && b_local && x_local && b_local != x_local, "V-cycle needs distinct buffers");
+    need(h->m->hierarchy() != nullptr, "the march was created without a preconditioner");
+    h->m->hierarchy()->vcycle(b_local, x_local, stream_of(stream));
+  });
+}
+int fde_dist_march_collectives(fde_dist_march h, unsigned long long* n) {
+  return guard([&] {
+    need(h && n, "null argument");
+    *n = h->m->comm().collectives();
+  });
+}
+int fde_dist_march_destroy(fde_dist_march h) {
+  delete h;
+  return FDE_OK;
+}
+
+int fde_vdist_run(const fde_problem* p, size_t n1, size_t n2, size_t steps,
+                  const fde_driver_config* cfg, int nranks, size_t agglomerate, int what,
+                  size_t nrun, const double* in_full, double* out_full, size_t* iterations,
+                  double* residuals, unsigned long long* collectives) {
+  return guard([&] {
+    need(cfg && out_full, "null argument");
+    need(what >= 0 && what <= 2, "what must be 0 (march), 1 (apply) or 2 (V-cycle)");
+    need(what == 0 || in_full, "apply / V-cycle need an input vector");
+    need(cfg->solver == 0 && (cfg->precond == PC_NONE || cfg->precond == PC_MGM),
+         "the y-slab march runs GMRES with none / mgm");
+    need(what != 2 || cfg->precond == PC_MGM, "V-cycle needs precond mgm");
+    const Problem prob = to_problem(p);
+    auto comms = make_virtual_comms(nranks);
+    const int dev = current_device();
+    cudaStream_t s = nullptr;
+    FDE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    std::vector<std::string> errs(nranks);
+    std::vector<int> codes(nranks, 0);
+    std::vector<std::thread> th;
+    for (int r = 0; r < nranks; ++r)
+      th.emplace_back([&, r] {
+        try {
+          FDE_CUDA(cudaSetDevice(dev));
+          DistMarch m(comms[r], prob, n1, n2, steps, solver_cfg_of(cfg), cfg->omega, cfg->coarse,
+                      cfg->coarse_sweeps, agglomerate, cfg->precond == PC_MGM);
+          const size_t nl = m.local_size(), off = m.r0() * n1;
+          DevBuf<double> a(nl + 1), b(nl + 1);
+          const double* res = nullptr;
+          if (what == 0) {
+            for (size_t k = 0; k < nrun; ++k) {
+              const DistReport rep = m.step(nullptr, s);
+              if (r == 0 && iterations) iterations[k] = rep.iterations;
+              if (r == 0 && residuals) residuals[k] = rep.final_rel;
+            }
+            res = m.solution();
+          } else {
+            FDE_CUDA(cudaMemcpyAsync(a.get(), in_full + off, nl * sizeof(double),
+                                     cudaMemcpyHostToDevice, s));
+            if (what == 1) m.level().run(a.get(), b.get(), 1.0, EPI_STORE, EpiArgs{}, s);
+            else m.hierarchy()->vcycle(a.get(), b.get(), s);
+            res = b.get();
+          }
+          FDE_CUDA(cudaMemcpyAsync(out_full + off, res, nl * sizeof(double),
+                                   cudaMemcpyDeviceToHost, s));
+          FDE_CUDA(cudaStreamSynchronize(s));
+          if (r == 0 && collectives) *collectives = m.comm().collectives();
+        } catch (const InvalidArgument& e) {
+          errs[r] = e.what();
+          codes[r] = 1;
+          abort_virtual(*comms[r]);
+        } catch (const std::exception& e) {
+          errs[r] = e.what();
+          codes[r] = 2;
+          abort_virtual(*comms[r]);
+        }
+      });
+    for (auto& t : th) t.join();
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    for (int r = 0; r < nranks; ++r)
+      if (codes[r] == 1 && errs[r] != "a virtual rank failed") throw InvalidArgument(errs[r]);
+    for (int r = 0; r < nranks; ++r)
+      if (codes[r]) throw RuntimeError("virtual rank " + std::to_string(r) + ": " + errs[r]);
   });
 }
 

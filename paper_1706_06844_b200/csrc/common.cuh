@@ -80,6 +80,22 @@ __device__ __forceinline__ void pdl_enter() {
 #endif
 }
 bool pdl_enabled();
+// Plain (fully serialised) launches while a PdlOff is alive on this thread.
+// The multi-GPU path interleaves kernels with copy-engine nodes (virtual-rank
+// device copies, small host<->device scalar copies): a kernel launched with
+// programmatic serialization right after such a node was observed to start
+// before the copy had landed (GMRES coefficients read stale; FDE_PDL=0 or
+// this scope removes it), and NCCL kernels never trigger early anyway.
+inline int& pdl_off_depth() {
+  static thread_local int depth = 0;
+  return depth;
+}
+struct PdlOff {
+  PdlOff() { ++pdl_off_depth(); }
+  ~PdlOff() { --pdl_off_depth(); }
+  PdlOff(const PdlOff&) = delete;
+  PdlOff& operator=(const PdlOff&) = delete;
+};
 
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -93,7 +109,7 @@ inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = (pdl_enabled() && pdl_off_depth() == 0) ? 1 : 0;
   cuda_check(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "kernel launch");
 }
 

@@ -100,7 +100,7 @@ def dram_traffic_in_run(local: int):
         for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
             env.pop(k, None)
         cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control",
-               "none", "-k", "regex:line_kernel|transpose|FillFunctor", "--csv", "--log-file",
+               "none", "--cache-control", "none", "-k", "regex:line_kernel|transpose|elementwise", "--csv", "--log-file",
                str(csvf), sys.executable, str(ROOT / "tools" / "traffic_probe.py"), str(N), "3"]
         try:
             r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=240)

@@ -333,6 +333,12 @@ int fde_dist_march_vcycle(fde_dist_march h, const double* b_local, double* x_loc
 /* collectives issued so far (all-to-all, all-gather, halo exchanges) */
 int fde_dist_march_collectives(fde_dist_march h, unsigned long long* n);
 int fde_dist_march_destroy(fde_dist_march h);
+/* The partition (host only, no device needed): balanced row offsets[0..nranks]
+ * of the fine level, and the offsets a coarser level inherits (coarse row b
+ * goes to the rank that owns its centre fine row 2b + 1 - par). */
+int fde_dist_split_rows(size_t n, int nranks, size_t* offsets);
+int fde_dist_induced_rows(const size_t* fine_offsets, int nranks, size_t d2, int coarsen_y,
+                          size_t* coarse_offsets);
 /* The same code on `nranks` VIRTUAL ranks of the current device (one host
  * thread per rank, one shared stream, collectives as ordered device copies):
  * how the N > 1 paths are exercised on one GPU.  HOST vectors of the whole

@@ -167,6 +167,9 @@ _SIGS = {
     "fde_dist_march_vcycle": (_c_int, [_c_vp, _c_vp, _c_vp, _c_vp]),
     "fde_dist_march_collectives": (_c_int, [_c_vp, ctypes.POINTER(ctypes.c_ulonglong)]),
     "fde_dist_march_destroy": (_c_int, [_c_vp]),
+    "fde_dist_split_rows": (_c_int, [_c_size, _c_int, ctypes.POINTER(_c_size)]),
+    "fde_dist_induced_rows": (_c_int, [ctypes.POINTER(_c_size), _c_int, _c_size, _c_int,
+                                       ctypes.POINTER(_c_size)]),
     "fde_vdist_run": (_c_int, [ctypes.POINTER(_FdeProblem), _c_size, _c_size, _c_size,
                                ctypes.POINTER(_DriverConfig), _c_int, _c_size, _c_int, _c_size,
                                _c_vp, _c_vp, ctypes.POINTER(_c_size), _c_vp,

@@ -978,6 +978,22 @@ int fde_dist_march_collectives(fde_dist_march h, unsigned long long* n) {
     *n = h->m->comm().collectives();
   });
 }
+int fde_dist_split_rows(size_t n, int nranks, size_t* offsets) {
+  return guard([&] {
+    need(offsets && nranks > 0, "bad arguments");
+    const auto o = split_ranges(n, nranks);
+    for (int r = 0; r <= nranks; ++r) offsets[r] = o[r];
+  });
+}
+int fde_dist_induced_rows(const size_t* fine_offsets, int nranks, size_t d2, int coarsen_y,
+                          size_t* coarse_offsets) {
+  return guard([&] {
+    need(fine_offsets && coarse_offsets && nranks > 0, "bad arguments");
+    const std::vector<size_t> f(fine_offsets, fine_offsets + nranks + 1);
+    const auto o = induced_coarse_rows(f, d2, coarsen_y != 0);
+    for (int r = 0; r <= nranks; ++r) coarse_offsets[r] = o[r];
+  });
+}
 int fde_dist_march_destroy(fde_dist_march h) {
   delete h;
   return FDE_OK;

@@ -797,9 +797,16 @@ constexpr int partner_slot(int s, bool t0) {
 // aligned in all streams -- bulk copies, 128-bit loads and 128-bit stores
 // apply to odd lines too (n + 1 <= M is checked by the host).
 // Pointers below address virtual position 0 (= element -sx).
+#ifndef FDE_L2_STREAM
+#define FDE_L2_STREAM 1  // evict_first hints on the coefficient streams
+#endif
+template <bool STREAM = false>
 __device__ __forceinline__ double2 ld_pair(const double* v0, int pv, int sx, int nv) {
   const double* a = v0 + pv;
-  if (pv >= sx && pv + 1 < nv) return __ldcg(reinterpret_cast<const double2*>(a));
+  if (pv >= sx && pv + 1 < nv) {
+    if constexpr (STREAM && FDE_L2_STREAM) return ldcg_stream(reinterpret_cast<const double2*>(a));
+    else return __ldcg(reinterpret_cast<const double2*>(a));
+  }
   double2 r = make_double2(0.0, 0.0);  // edge pairs: element by element
   if (pv >= sx && pv < nv) r.x = __ldcg(a);
   if (pv + 1 < nv) r.y = __ldcg(a + 1);
@@ -834,7 +841,9 @@ struct LineIO<YPass, EPI> {
   size_t n1;
   double c;
   int sx, nv;
+  uint64_t pol;  // L2 evict_last policy for the Q stores (0: plain stores)
   __device__ __forceinline__ LineIO(const YPass& p, int line, int sx_) {
+    pol = p.keep_q ? l2_policy_evict_last() : 0;
     const ptrdiff_t o = (ptrdiff_t)line * p.n2 - sx_;
     sx = sx_;
     nv = p.n2 + sx_;
@@ -850,7 +859,9 @@ struct LineIO<YPass, EPI> {
   struct Glob {
     double2 s1;
   };
-  __device__ __forceinline__ Glob fetch_glob(int pv) const { return Glob{ld_pair(em, pv, sx, nv)}; }
+  __device__ __forceinline__ Glob fetch_glob(int pv) const {
+    return Glob{ld_pair<true>(em, pv, sx, nv)};
+  }
   __device__ __forceinline__ void prefetch_rest(uint32_t) const {}
   __device__ __forceinline__ void finish(int pv, bool live, double2 ty, double2 tt, double2 s0,
                                          const Glob& g) const {
@@ -859,8 +870,13 @@ struct LineIO<YPass, EPI> {
     if (QT) {
       st_pair(q, pv, sx, nv, live, v);
     } else if (live) {
-      if (pv >= sx && pv < nv) q[(size_t)pv * n1] = v.x;
-      if (pv + 1 < nv) q[(size_t)(pv + 1) * n1] = v.y;
+      if (pol) {
+        if (pv >= sx && pv < nv) st_l2_hint(q + (size_t)pv * n1, v.x, pol);
+        if (pv + 1 < nv) st_l2_hint(q + (size_t)(pv + 1) * n1, v.y, pol);
+      } else {
+        if (pv >= sx && pv < nv) q[(size_t)pv * n1] = v.x;
+        if (pv + 1 < nv) q[(size_t)(pv + 1) * n1] = v.y;
+      }
     }
   }
 };
@@ -902,8 +918,8 @@ struct LineIO<XPass, EPI> {
   };
   __device__ __forceinline__ Glob fetch_glob(int pv) const {
     Glob g;
-    g.s1 = ld_pair(dm, pv, sx, nv);
-    g.x = ld_pair(x, pv, sx, nv);
+    g.s1 = ld_pair<true>(dm, pv, sx, nv);
+    g.x = ld_pair<true>(x, pv, sx, nv);  // last read of x by this apply
     g.q = q ? ld_pair(q, pv, sx, nv) : make_double2(0.0, 0.0);
     g.e1 = EPI == EPI_STORE ? make_double2(0.0, 0.0) : ld_pair(e1, pv, sx, nv);
     g.e2 = EPI == EPI_JACOBI ? ld_pair(e2, pv, sx, nv) : make_double2(0.0, 0.0);
@@ -1026,8 +1042,9 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CT
   // both mbarriers complete once per line: their phase parity rides in bit 30
   // of the loop counter (one loop-carried register instead of two; a spilled
   // parity word cost an exposed local-memory load before every wait)
+  int st = vb * LPC;
 #pragma unroll 1
-  for (int st = vb * LPC; (st & 0x3fffffff) < nl; st = (st + nvb * LPC) ^ 0x40000000) {
+  for (; (st & 0x3fffffff) < nl; st = (st + nvb * LPC) ^ 0x40000000) {
     const int base = st & 0x3fffffff;
     const uint32_t phase = (uint32_t)st >> 30;
     const int line = line_of(base);
@@ -1053,8 +1070,13 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CT
 #if FDE_BULK_PF
       if (tl == 0) {  // this line's operand streams and the next line's input -> L2
         const uint32_t bytes = chunks_of(line, false) * 16;
+#if FDE_L2_STREAM
+        bulk_prefetch_l2_stream(io.staged(0), bytes);
+        bulk_prefetch_l2_stream(io.staged(1), bytes);
+#else
         bulk_prefetch_l2(io.staged(0), bytes);
         bulk_prefetch_l2(io.staged(1), bytes);
+#endif
         io.prefetch_rest(chunks_of(line, true) * 16);
         if (next < nl) {
           const int ln = line_of(next);
@@ -1064,10 +1086,24 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CT
 #endif
     }
 
+    // the transposed-input scratch was read for the last time by this line's
+    // bulk copy: drop its L2 lines instead of writing them back
+    if constexpr (std::is_same<Pol, YPass>::value) {
+      if (p.scratch_x && live && line != nl - 1)
+        l2_discard_range(p.x + (size_t)line * p.n2, n, tl, T);
+    }
+
     // 2) forward transform; ends with this thread's paired slots in v
     double2 w1s[P];
     double2* const xbuf = reinterpret_cast<double2*>(smem);  // exchange slots
     PFwd<LOGM, P, 0, true>::run(v, xbuf, tl, p.blk.twM, w1s, [] {});
+    // the previous line's Q (row pass): every thread of the group is past its
+    // epilogue loads (the forward transform's barriers), so its lines can go
+    if constexpr (std::is_same<Pol, XPass>::value) {
+      const int pb = base - nvb * LPC;  // the group's previous lines
+      if (p.scratch_q && p.q && pb >= vb * LPC && pb + ls < nl)
+        l2_discard_range(p.q + (size_t)(pb + ls) * p.n1, n, tl, T);
+    }
 
     // 3) spectral step (see fft_line_kernel): partners are in registers;
     //    results go to tensor memory in groups of 4 slots.  With
@@ -1134,7 +1170,11 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CT
           const uint32_t bytes = chunks_of(line, false) * 16;
           fence_proxy_async();
           mbar_expect_tx(bar_c, bytes);
+#if FDE_L2_STREAM
+          bulk_g2s_stream(smem, IO(p, line, sx).staged(0), bytes, bar_c);
+#else
           bulk_g2s(smem, IO(p, line, sx).staged(0), bytes, bar_c);
+#endif
           if (next < nl) issue_input(line_of(next));
         }
       };
@@ -1185,6 +1225,11 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CT
   }
   tmem_fence_before();
   __syncthreads();
+  if constexpr (std::is_same<Pol, XPass>::value) {
+    const int pb = (st & 0x3fffffff) - nvb * LPC;  // the group's last lines
+    if (p.scratch_q && p.q && pb >= vb * LPC && pb + ls < nl)
+      l2_discard_range(p.q + (size_t)(pb + ls) * p.n1, n, tl, T);
+  }
   if (warp == 0) tmem_dealloc<S::TCOLS_CTA>(tbase);
 }
 
@@ -1243,18 +1288,20 @@ __global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict
                                                         double* __restrict__ out, int n1, int n2) {
   pdl_enter();
   __shared__ double tile[32][33];
+  const uint64_t pol = l2_policy_evict_last();  // the transposed copy is read next, once
   const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < 32; k += 8) {
     const int i = i0 + tx, j = j0 + ty + k;
-    if (i < n1 && j < n2) tile[ty + k][tx] = in[(size_t)j * n1 + i];
+    // the row pass reads x again: keep it in L2 over the column pass
+    if (i < n1 && j < n2) tile[ty + k][tx] = ld_l2_hint(in + (size_t)j * n1 + i, pol);
   }
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < 32; k += 8) {
     const int j = j0 + tx, i = i0 + ty + k;
-    if (i < n1 && j < n2) out[(size_t)i * n2 + j] = tile[tx][ty + k];
+    if (i < n1 && j < n2) st_l2_hint(out + (size_t)i * n2 + j, tile[tx][ty + k], pol);
   }
 }
 
@@ -1266,6 +1313,7 @@ __global__ void __launch_bounds__(256) transpose_map_kernel(const InMap m, doubl
                                                             int n2) {
   pdl_enter();
   __shared__ double tile[32][33];
+  const uint64_t pol = l2_policy_evict_last();
   const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
 #pragma unroll
@@ -1281,7 +1329,7 @@ __global__ void __launch_bounds__(256) transpose_map_kernel(const InMap m, doubl
 #pragma unroll
   for (int k = 0; k < 32; k += 8) {
     const int j = j0 + tx, i = i0 + ty + k;
-    if (i < n1 && j < n2) out[(size_t)i * n2 + j] = tile[tx][ty + k];
+    if (i < n1 && j < n2) st_l2_hint(out + (size_t)i * n2 + j, tile[tx][ty + k], pol);
   }
 }
 

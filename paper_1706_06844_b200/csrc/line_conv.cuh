@@ -94,6 +94,8 @@ struct YPass {
   double* q;          // Q[i + j * n1], or Q transposed (Q[i * n2 + j]) when qT is set
   int qT;
   int par = 0;        // set by the launcher: common base-address parity (line_conv.cu)
+  int scratch_x = 0;  // x is library scratch read once: its L2 lines are discarded after the read
+  int keep_q = 0;     // Q is read once by the row pass that follows: stored evict_last
   __device__ __forceinline__ int nlines() const { return n1; }
   __device__ __forceinline__ double load(int line, int pos) const {
     return xT ? x[(size_t)line * n2 + pos] : x[(size_t)pos * n1 + line];
@@ -145,6 +147,7 @@ struct XPass {
   const double* src;   // EPI_RHS
   double src_scale;
   int par = 0;         // set by the launcher: common base-address parity (line_conv.cu)
+  int scratch_q = 0;   // q is library scratch read once: its L2 lines are discarded after the read
   __device__ __forceinline__ int nlines() const { return n2; }
   __device__ __forceinline__ double load(int line, int pos) const {
     return x[(size_t)line * n1 + pos];

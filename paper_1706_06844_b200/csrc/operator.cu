@@ -315,6 +315,11 @@ void StructuredOp::sync_host(cudaStream_t s) {
 
 // FFT-path column passes read a transposed copy of the input from this many
 // columns up (fewer columns: strided gathers, one transpose launch saved)
+// L2 residency of the transposed-input and Q scratch (tmem.cuh): evict_last
+// stores, discard after the single read
+#ifndef FDE_L2_SCRATCH
+#define FDE_L2_SCRATCH 1
+#endif
 #ifndef FDE_XT_MIN
 #define FDE_XT_MIN 512  // measured: 128 or 256 (-0.4 to -1 %), 1024 (-0.3 %) slower
 #endif
@@ -347,11 +352,14 @@ void StructuredOp::run_impl(const InMap* in, const double* x, double* out, doubl
     launch_transpose_mapped(*in, const_cast<double*>(x), d_xT_.get(), (int)n1_, (int)n2_, s);
     yp.x = d_xT_.get();
     yp.xT = 1;
+    yp.scratch_x = FDE_L2_SCRATCH;
   } else if (maps_input()) {
     launch_transpose(x, d_xT_.get(), (int)n1_, (int)n2_, s);
     yp.x = d_xT_.get();
     yp.xT = 1;
+    yp.scratch_x = FDE_L2_SCRATCH;
   }
+  yp.keep_q = FDE_L2_SCRATCH;
   yp.epT = d_epT_.get();
   yp.emT = d_emT_.get();
   yp.c = sign * s_over_r_;
@@ -376,6 +384,7 @@ void StructuredOp::run_impl(const InMap* in, const double* x, double* out, doubl
   xp.dp = d_dp_.get();
   xp.dm = d_dm_.get();
   xp.q = d_q_.get();
+  xp.scratch_q = FDE_L2_SCRATCH;
   xp.inv_r = inv_r_;
   xp.sign = sign;
   xp.epi = epi;

@@ -153,6 +153,63 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* gsrc, uint32_t byte
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gsrc), "r"(bytes) : "memory");
 }
 
+// ---- L2 residency of the library's scratch streams ---------------------------
+// The transposed input and the column-pass result Q are written by one kernel
+// and read once by the next: stored with an evict_last policy they stay in
+// the 126 MB L2 across the kernel boundary, and once consumed their lines are
+// discarded (no write-back), so neither scratch costs DRAM traffic.
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// streamed-once operands (coefficient lines): first to go, so they do not
+// push the evict_last scratch out
+__device__ __forceinline__ void bulk_g2s_stream(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                                uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+      "l"(gsrc), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+      "l"(l2_policy_evict_first())
+      : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2_stream(const void* gsrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(gsrc),
+               "r"(bytes), "l"(l2_policy_evict_first())
+               : "memory");
+}
+__device__ __forceinline__ double2 ldcg_stream(const double2* a) {
+  double2 r;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(a), "l"(l2_policy_evict_first()));
+  return r;
+}
+__device__ __forceinline__ double ld_l2_hint(const double* a, uint64_t pol) {
+  double r;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(a), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void st_l2_hint(double* a, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+// Drop the whole 128-byte L2 lines inside [base, base + n) doubles (lines that
+// straddle the ends belong partly to a neighbour and are left alone);
+// `tid` of `nthreads` threads share the work.  The range must have been read
+// for the last time.
+__device__ __forceinline__ void l2_discard_range(const double* base, int n, int tid, int nthreads) {
+  const uintptr_t b = reinterpret_cast<uintptr_t>(base), e = b + (uintptr_t)n * 8;
+  const uintptr_t lo = (b + 127) & ~(uintptr_t)127, hi = e & ~(uintptr_t)127;
+  for (uintptr_t a = lo + (uintptr_t)tid * 128; a < hi; a += (uintptr_t)nthreads * 128)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+}
+
 // ---- cp.async (LDGSTS) helpers: global -> shared without registers --------
 // 8-byte copy; src_bytes = 0 zero-fills the destination (address must still be valid)
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, int src_bytes) {

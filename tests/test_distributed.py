@@ -149,3 +149,28 @@ def test_partition_helpers():
     assert D.induced_coarse_rows([0, 4, 9], 9, True) == [0, 2, 4]
     assert D.induced_coarse_rows([0, 5, 10], 10, True) == [0, 3, 5]  # par 1: centres 0,2,4,6,8
     assert D.induced_coarse_rows([0, 4, 9], 9, False) == [0, 4, 9]
+
+
+def test_cxx_partition_matches_python():
+    """The C++ march's row partition (csrc/dist.cu) equals the Python
+    emulation's for every level of random plans (host only)."""
+    import ctypes
+    import paper_1706_06844_b200 as fde
+    from paper_1706_06844_b200 import distributed as D
+    lib = fde.load_library()
+    rng = np.random.default_rng(0)
+    for _ in range(300):
+        P = int(rng.integers(1, 9))
+        d2 = int(rng.integers(2 * P, 5000))
+        arr = (ctypes.c_size_t * (P + 1))()
+        assert lib.fde_dist_split_rows(d2, P, arr) == 0
+        rows = [int(v) for v in arr]
+        assert rows == D.split_ranges(d2, P)
+        while d2 >= 4:
+            for cy in (1, 0):
+                out = (ctypes.c_size_t * (P + 1))()
+                assert lib.fde_dist_induced_rows(arr, P, d2, cy, out) == 0
+                assert [int(v) for v in out] == D.induced_coarse_rows(rows, d2, bool(cy)), (rows, d2, cy)
+            rows = D.induced_coarse_rows(rows, d2, True)
+            arr = (ctypes.c_size_t * (P + 1))(*rows)
+            d2 = D.coarse_size(d2)

@@ -53,7 +53,7 @@ def test_apply_fullsize_vs_oracle(cuda, orc, cfg, n):
     assert rel(op.apply_rhs(dev(x)).cpu().numpy(), orc.apply(s, x, -1)) <= 1e-13
 
 
-@pytest.mark.parametrize("cfg,n", [(4, 2047), (5, 2047), (3, 1023)])
+@pytest.mark.parametrize("cfg,n", [(4, 2047), (5, 2047), (3, 1023), (5, 4095)])
 def test_vcycle_fullsize_vs_oracle(cuda, orc, cfg, n):
     s = spec(cfg, n1=n, n2=n, steps=8)
     p = fde.Problem.preset_config(cfg, steps=8)
@@ -225,3 +225,17 @@ def test_cfg5_largest_grid_n8191(cuda, orc):
     v12 = 3.0 * h.vcycle(b1) - h.vcycle(b2)
     assert bool(torch.isfinite(v).all())
     assert float(torch.linalg.norm(v - v12) / torch.linalg.norm(v)) <= 1e-12
+
+
+def test_cfg5_n8191_apply_full_vector_vs_oracle(cuda, orc):
+    """cfg5's largest grid: every one of the 67 M outputs of one operator apply
+    against the oracle's FFT apply (the sampled direct-sum check above pins
+    the oracle's answer there)."""
+    n = 8191
+    s = spec(5, n1=n, n2=n, steps=1)
+    p = fde.Problem.preset_config(5, steps=1)
+    op = fde.StructuredFdeOperator.assemble(p, n, n, 1, 1)
+    x = np.random.default_rng(5).uniform(-1, 1, n * n)
+    y = op.apply(dev(x)).cpu().numpy()
+    del op
+    assert rel(y, orc.apply(s, x)) <= 1e-13

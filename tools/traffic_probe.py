@@ -32,26 +32,31 @@ def parse(path):
     for r in rows[hdr + 1:]:
         if len(r) <= iv or not r[iid].isdigit():
             continue
-        d = launches.setdefault(int(r[iid]), {"name": r[ik], "bytes": 0.0})
+        d = launches.setdefault(int(r[iid]), {"name": r[ik], "bytes": 0.0, "rd": 0.0, "wr": 0.0})
         if r[im] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            d["bytes"] += float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
+            v = float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
+            d["bytes"] += v
+            d["rd" if "read" in r[im] else "wr"] += v
     seq = [launches[k] for k in sorted(launches)]
     is_apply = lambda d: ("line_kernel" in d["name"]) or ("transpose" in d["name"])
     # flush alone: a non-apply launch that follows another non-apply launch
     alone = [b["bytes"] for a, b in zip(seq, seq[1:]) if not is_apply(a) and not is_apply(b)]
     if not alone:
-        raise SystemExit("no standalone flush launch in the capture")
+        raise ValueError("no standalone flush launch in the capture")
     base = alone[-1]
     per_apply, kernels, cur, names = [], [], 0.0, []
     for d in seq:
         if is_apply(d):
             cur += d["bytes"]
-            names.append(d["name"].split("(")[0].split("::")[-1][:48])
+            names.append({"kernel": d["name"].split("(")[0].split("::")[-1][:48],
+                          "read_MB": round(d["rd"] / 1e6, 1), "write_MB": round(d["wr"] / 1e6, 1)})
         elif names:
             per_apply.append(cur + d["bytes"] - base)
+            names.append({"kernel": "write-back during the following flush",
+                          "extra_MB": round((d["bytes"] - base) / 1e6, 1)})
             kernels, cur, names = names, 0.0, []
     if not per_apply:
-        raise SystemExit("no apply in the capture")
+        raise ValueError("no apply in the capture")
     per_apply.sort()
     return {"bytes_per_apply": per_apply[len(per_apply) // 2], "applies": len(per_apply),
             "flush_alone_bytes": base, "kernels_per_apply": kernels}

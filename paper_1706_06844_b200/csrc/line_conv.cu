@@ -975,8 +975,11 @@ constexpr int paired_pts_for(bool ypass) {
 template <int LOGM, class Pol>
 constexpr int paired_pts() { return paired_pts_for<LOGM>(std::is_same<Pol, YPass>::value); }
 template <int LOGM, class Pol, int EPI>
+#ifndef FDE_PAIRED_CTAS
+#define FDE_PAIRED_CTAS 4  // resident 128-thread CTAs per SM the register budget is cut for
+#endif
 __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CTA_THREADS,
-                                  512 / PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CTA_THREADS)
+                                  FDE_PAIRED_CTAS * 128 / PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CTA_THREADS)
     fft_line_kernel_paired(const Pol p) {
   pdl_enter();
   constexpr int P = paired_pts<LOGM, Pol>();

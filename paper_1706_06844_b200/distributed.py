@@ -1,4 +1,10 @@
-"""Multi-GPU CN-WSGD time step by y-slab decomposition.
+"""Python statement of the y-slab multi-GPU time step.
+
+The product path is C++ (csrc/dist.cu behind fde_dist_* / fde.SlabMarch, NCCL,
+or virtual ranks on one GPU).  This module states the same algorithm over a
+backend interface; tests/test_distributed.py runs it on a numpy backend with
+gloo at world size 2 and 3 on CPU (partition, halo rules, GMRES control flow)
+and tests/test_gpu_distributed.py on the library's slab kernels at world 1.
 
 One process per GPU.  Rank r owns grid rows [r0, r1) of every multigrid level
 (x index fastest, so a row is n1 contiguous doubles):

@@ -62,8 +62,10 @@ struct fde_march_s {
   // pipelined host I/O (fde_march_prefetch_source / _solution_async)
   cudaStream_t cs = nullptr;            // copy stream
   cudaEvent_t ev_step = nullptr;        // u^m final on the compute stream
-  cudaEvent_t ev_d2h = nullptr;         // last D2H of a solution buffer done
-  const double* d2h_buf = nullptr;      // the buffer that D2H reads
+  // u and x swap between the same two allocations: one event per allocation,
+  // recorded after the last D2H that reads it
+  cudaEvent_t ev_d2h[2] = {};
+  const double* d2h_buf[2] = {nullptr, nullptr};
   // prefetched sources: a ring of three device buffers, up to two in flight
   DevBuf<double> ring[3];
   cudaEvent_t ev_ready[3] = {};  // H2D into ring[i] done (copy stream)
@@ -75,7 +77,7 @@ struct fde_march_s {
     if (cs) return;
     FDE_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     FDE_CUDA(cudaEventCreateWithFlags(&ev_step, cudaEventDisableTiming));
-    FDE_CUDA(cudaEventCreateWithFlags(&ev_d2h, cudaEventDisableTiming));
+    for (cudaEvent_t& e : ev_d2h) FDE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (int i = 0; i < 3; ++i) {
       FDE_CUDA(cudaEventCreateWithFlags(&ev_ready[i], cudaEventDisableTiming));
       FDE_CUDA(cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming));
@@ -86,7 +88,7 @@ struct fde_march_s {
       cudaStreamSynchronize(cs);
       cudaStreamDestroy(cs);
       cudaEventDestroy(ev_step);
-      cudaEventDestroy(ev_d2h);
+      for (cudaEvent_t e : ev_d2h) cudaEventDestroy(e);
       for (int i = 0; i < 3; ++i) {
         cudaEventDestroy(ev_ready[i]);
         cudaEventDestroy(ev_free[i]);
@@ -660,11 +662,14 @@ int fde_march_step(fde_march h, const double* source, int source_mode, void* str
     } else {
       throw InvalidArgument("source_mode must be 0, 1, 2 or 3");
     }
-    // the solve overwrites h->x: any solution copy still in flight must finish
-    // first.  ev_d2h is the LAST copy on the (in-order) copy stream, so it
-    // covers every earlier one too -- two back-to-back asynchronous reads leave
-    // both u^m buffers pending, not just the most recent.
-    if (h->cs && h->d2h_buf) FDE_CUDA(cudaStreamWaitEvent(s, h->ev_d2h, 0));
+    // the solve overwrites h->x: a solution copy that still reads THAT
+    // allocation must finish first (u and x alternate between two allocations,
+    // each with its own event, recorded after the last copy that reads it).
+    // The copy of u^{m-1} reads h->u, which this step only reads: no wait, so
+    // the D2H of one step overlaps the next step's solve.
+    if (h->cs)
+      for (int i = 0; i < 2; ++i)
+        if (h->d2h_buf[i] == h->x.get()) FDE_CUDA(cudaStreamWaitEvent(s, h->ev_d2h[i], 0));
     // assemble_rhs (problem.cpp:73-89): b = apply_rhs(u) + 2 hx^alpha v, fused
     EpiArgs e;
     e.src = src;
@@ -731,8 +736,10 @@ int fde_march_solution_async(fde_march h, double* host_u) {
     FDE_CUDA(cudaStreamWaitEvent(h->cs, h->ev_step, 0));  // u^m written by the last step
     FDE_CUDA(cudaMemcpyAsync(host_u, h->u.get(), h->g.size() * sizeof(double),
                              cudaMemcpyDeviceToHost, h->cs));
-    FDE_CUDA(cudaEventRecord(h->ev_d2h, h->cs));
-    h->d2h_buf = h->u.get();
+    // slot of this allocation (only two exist: slot 1 is the other one's or free)
+    const int slot = (h->d2h_buf[0] == h->u.get() || h->d2h_buf[0] == nullptr) ? 0 : 1;
+    FDE_CUDA(cudaEventRecord(h->ev_d2h[slot], h->cs));
+    h->d2h_buf[slot] = h->u.get();
   });
 }
 

@@ -79,6 +79,16 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
 }
+__device__ __forceinline__ void pdl_launch_dependents() {
+#if defined(__CUDA_ARCH__)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_wait() {
+#if defined(__CUDA_ARCH__)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
 bool pdl_enabled();
 // Plain (fully serialised) launches while a PdlOff is alive on this thread.
 // The multi-GPU path interleaves kernels with copy-engine nodes (virtual-rank

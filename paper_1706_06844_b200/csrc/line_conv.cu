@@ -974,6 +974,8 @@ constexpr int paired_pts_for(bool ypass) {
 }
 template <int LOGM, class Pol>
 constexpr int paired_pts() { return paired_pts_for<LOGM>(std::is_same<Pol, YPass>::value); }
+__device__ __forceinline__ bool late_wait_of(const YPass&) { return false; }
+__device__ __forceinline__ bool late_wait_of(const XPass& p) { return p.late_wait != 0; }
 template <int LOGM, class Pol, int EPI>
 #ifndef FDE_PAIRED_CTAS
 #define FDE_PAIRED_CTAS 4  // resident 128-thread CTAs per SM the register budget is cut for
@@ -981,7 +983,14 @@ template <int LOGM, class Pol, int EPI>
 __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CTA_THREADS,
                                   FDE_PAIRED_CTAS * 128 / PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CTA_THREADS)
     fft_line_kernel_paired(const Pol p) {
-  pdl_enter();
+  // Row pass behind a column pass that holds every tensor-memory column of
+  // every SM (p.late_wait, see launch_paired_epi): nothing before the
+  // epilogue depends on the column pass, so the wait for it moves there and
+  // this grid's first lines run in the slots the column pass's early
+  // finishers leave (2047 lines on 592 slots: the last round is half empty).
+  pdl_launch_dependents();
+  const bool late_wait = late_wait_of(p);
+  if (!late_wait) pdl_wait();
   constexpr int P = paired_pts<LOGM, Pol>();
   using S = PairedShape<LOGM, P>;
   using IO = LineIO<Pol, EPI>;
@@ -1205,6 +1214,7 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CT
 #pragma unroll
         for (int c = 0; c < G; ++c) gl[c] = io.fetch_glob(2 * (tl + (g + c) * T));
       };
+      if (late_wait) pdl_wait();  // Q (and everything older) is complete and visible
       fetch_group(0);
       mbar_wait(bar_c, phase);
 #pragma unroll
@@ -1342,7 +1352,7 @@ int lines_of(const P& p) {
 }
 
 template <int LOGM, class P>
-void launch_fft(const P& p, cudaStream_t s) {
+bool launch_fft(const P& p, cudaStream_t s) {
   using S = FftShape<LOGM>;
   // per template instance and device: opt-in shared memory, SM count
   static DeviceCache<int> sm_count;
@@ -1363,6 +1373,7 @@ void launch_fft(const P& p, cudaStream_t s) {
   const size_t smem = size_t(lpb) * 2 * S::BUF * sizeof(double);
   launch_k(fft_line_kernel<LOGM, P>, grid, S::T * lpb, smem, s, p);
   FDE_LAUNCH_CHECK();
+  return false;
 }
 
 #ifndef FDE_PAIRED
@@ -1400,8 +1411,11 @@ inline int paired_parity(const YPass& p) {
   return common_parity({p.x, p.epT, p.emT, p.qT ? p.q : nullptr});
 }
 
+// Returns true when the grid holds all 512 tensor-memory columns of every SM
+// until its first CTA exits: a paired kernel launched behind it cannot
+// allocate its own columns -- the first thing it does -- before then.
 template <int LOGM, class P, int EPI>
-void launch_paired_epi(const P& p, cudaStream_t s) {
+bool launch_paired_epi(const P& p, cudaStream_t s) {
   constexpr int PP = paired_pts<LOGM, P>();
   using S = PairedShape<LOGM, PP>;
   // resident CTAs on the device (persistent grid) and the shared-memory
@@ -1410,8 +1424,8 @@ void launch_paired_epi(const P& p, cudaStream_t s) {
   // the TMEM allocation).  What the carveout leaves of the SM's 256 KB is
   // L1: it keeps the spectral constants (64 KB per block at M = 2048) and
   // the twiddle tables resident across lines.
-  static DeviceCache<int> resident;
-  const int max_ctas = resident.get([](int dev) {
+  static DeviceCache<std::pair<int, bool>> resident;
+  const std::pair<int, bool> res = resident.get([](int dev) {
     int sms = 0, smem_sm = 0, smem_rsv = 0, regs_sm = 0;
     FDE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     FDE_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
@@ -1433,17 +1447,19 @@ void launch_paired_epi(const P& p, cudaStream_t s) {
     if (carve > 100) carve = 100;
     FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
                                   cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-    return sms * per_sm;
+    return std::make_pair(sms * per_sm, per_sm * S::TCOLS_CTA == 512);
   });
+  const int max_ctas = res.first;
   const int groups = (lines_of(p) + S::LPC - 1) / S::LPC;
   const int ctas = (groups + S::NG - 1) / S::NG;
   launch_k(fft_line_kernel_paired<LOGM, P, EPI>, ctas < max_ctas ? ctas : max_ctas,
            S::CTA_THREADS, S::SMEM, s, p);
   FDE_LAUNCH_CHECK();
+  return ctas >= max_ctas && res.second;
 }
 
 template <int LOGM, class P>
-void launch_paired(const P& p0, cudaStream_t s) {
+bool launch_paired(const P& p0, cudaStream_t s) {
   P p = p0;
   p.par = paired_parity(p);
   if (p.par < 0 || p.blk.n + 1 > (1 << LOGM)) return launch_fft<LOGM>(p0, s);
@@ -1461,14 +1477,14 @@ void launch_paired(const P& p0, cudaStream_t s) {
 }
 
 template <class P>
-void launch_any(const P& p, cudaStream_t s) {
+bool launch_any(const P& p, cudaStream_t s) {
   const int lines = lines_of(p);
-  if (lines <= 0) return;
+  if (lines <= 0) return false;
   switch (p.blk.logM) {
     case 0:
       launch_k(direct_line_kernel<P>, (lines + 7) / 8, 256, 0, s, p);
       FDE_LAUNCH_CHECK();
-      return;
+      return false;
     case 6: return launch_fft<6>(p, s);
     case 7: return launch_fft<7>(p, s);
     case 8: return FDE_PAIRED8 ? launch_paired<8>(p, s) : launch_fft<8>(p, s);
@@ -1484,7 +1500,7 @@ void launch_any(const P& p, cudaStream_t s) {
 
 }  // namespace
 
-void launch_line_pass(const YPass& p, cudaStream_t s) { launch_any(p, s); }
+bool launch_line_pass(const YPass& p, cudaStream_t s) { return launch_any(p, s); }
 void launch_transpose(const double* in, double* out, int n1, int n2, cudaStream_t s) {
   const dim3 grid((n1 + 31) / 32, (n2 + 31) / 32);
   launch_k(transpose_kernel, grid, 256, 0, s, in, out, n1, n2);
@@ -1501,6 +1517,6 @@ void launch_transpose_mapped(const InMap& m, double* xout, double* out, int n1, 
   }
   FDE_LAUNCH_CHECK();
 }
-void launch_line_pass(const XPass& p, cudaStream_t s) { launch_any(p, s); }
+bool launch_line_pass(const XPass& p, cudaStream_t s) { return launch_any(p, s); }
 
 }  // namespace fde_b200

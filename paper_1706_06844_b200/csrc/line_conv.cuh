@@ -148,6 +148,9 @@ struct XPass {
   double src_scale;
   int par = 0;         // set by the launcher: common base-address parity (line_conv.cu)
   int scratch_q = 0;   // q is library scratch read once: its L2 lines are discarded after the read
+  // the launch right before this one was the column pass that writes q and it
+  // reported a saturated grid (launch_line_pass): wait for it in the epilogue
+  int late_wait = 0;
   __device__ __forceinline__ int nlines() const { return n2; }
   __device__ __forceinline__ double load(int line, int pos) const {
     return x[(size_t)line * n1 + pos];
@@ -195,13 +198,15 @@ struct XPass {
   }
 };
 
-void launch_line_pass(const YPass& p, cudaStream_t s);
+// true: the grid keeps every SM's tensor memory allocated until its first CTA
+// exits (what XPass::late_wait needs from the launch before it)
+bool launch_line_pass(const YPass& p, cudaStream_t s);
 // out[i * n2 + j] = in[i + j * n1] (tiled through shared memory)
 void launch_transpose(const double* in, double* out, int n1, int n2, cudaStream_t s);
 // out[i * n2 + j] = v(i, j) = m.at(i, j), and xout[i + j * n1] = v(i, j) when
 // xout is set (it may alias m.a: each element is read and written by one thread)
 void launch_transpose_mapped(const InMap& m, double* xout, double* out, int n1, int n2,
                              cudaStream_t s);
-void launch_line_pass(const XPass& p, cudaStream_t s);
+bool launch_line_pass(const XPass& p, cudaStream_t s);
 
 }  // namespace fde_b200

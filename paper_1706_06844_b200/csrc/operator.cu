@@ -320,6 +320,10 @@ void StructuredOp::sync_host(cudaStream_t s) {
 #ifndef FDE_L2_SCRATCH
 #define FDE_L2_SCRATCH 1
 #endif
+// Row pass waits for the column pass only in its first epilogue (line_conv.cu)
+#ifndef FDE_LATE_WAIT
+#define FDE_LATE_WAIT 1
+#endif
 #ifndef FDE_XT_MIN
 #define FDE_XT_MIN 512  // measured: 128 or 256 (-0.4 to -1 %), 1024 (-0.3 %) slower
 #endif
@@ -374,7 +378,7 @@ void StructuredOp::run_impl(const InMap* in, const double* x, double* out, doubl
     launch_line_pass(yp, s);
   }
 #else
-  launch_line_pass(yp, s);
+  const bool y_saturates = launch_line_pass(yp, s);
 #endif
   XPass xp{};
   xp.blk = ax_.dev();
@@ -394,6 +398,9 @@ void StructuredOp::run_impl(const InMap* in, const double* x, double* out, doubl
   xp.omega = e.omega;
   xp.src = e.src;
   xp.src_scale = e.src_scale;
+#ifndef FDE_EXP_QTX
+  xp.late_wait = FDE_LATE_WAIT && y_saturates;
+#endif
   launch_line_pass(xp, s);
 }
 

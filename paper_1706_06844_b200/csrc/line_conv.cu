@@ -23,6 +23,29 @@ namespace {
 template <int SH>
 __device__ __forceinline__ int swz(int p) { return p ^ ((p >> SH) & 15); }
 
+// Programmatic-launch protocol of a column pass / row pass pair.  Nothing a
+// row pass does before its epilogue depends on the column pass (it transforms
+// x, the column pass writes Q), so a row pass launched right behind its column
+// pass (XPass::late_wait) waits for it only before its first epilogue: its
+// first lines run in the slots the column pass's early finishers leave (2047
+// lines on 592 slots: the last round is half empty), and on small levels the
+// two grids run side by side.  What it reads before that wait (x, coefficient
+// streams, through L2) was written by kernels BEFORE the column pass; the
+// column pass therefore lets its dependents launch only after its own wait,
+// i.e. once everything before it is complete and flushed.  Returns whether
+// the caller still owes the wait.
+__device__ __forceinline__ bool pass_enter(const YPass&) {
+  pdl_wait();
+  pdl_launch_dependents();
+  return false;
+}
+__device__ __forceinline__ bool pass_enter(const XPass& p) {
+  pdl_launch_dependents();
+  if (p.late_wait) return true;
+  pdl_wait();
+  return false;
+}
+
 // Spectral constants of one k from the compact table (operator.cu): a_k at
 // index k (k < M), b_c at M + c for c <= M/2; b_k = b_k (k <= M/2) or
 // -conj(b_{M-k}).  48 KB per block at M = 2048: together with the stage
@@ -375,7 +398,7 @@ struct FftShape {
 template <int LOGM, class Pol>
 __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
     fft_line_kernel(const Pol p) {
-  pdl_enter();
+  const bool late_wait = pass_enter(p);
   using S = FftShape<LOGM>;
   constexpr int M = S::M, T = S::T, BUF = S::BUF, P = S::P, H = P / 2, SH = Log2<P>::v;
   extern __shared__ double smem[];
@@ -398,7 +421,7 @@ __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
 #pragma unroll
   for (int s = 0; s < H; ++s) {
     const int i0 = 2 * (tl + s * T);
-    v[s].x = (active && i0 < n) ? p.load(line, i0) : 0.0;
+    v[s].x = (active && i0 < n) ? p.load(line, i0) : 0.0;  // (row pass: through L2, see pass_enter)
     v[s].y = (active && i0 + 1 < n) ? p.load(line, i0 + 1) : 0.0;
     v[s + H] = make_double2(0.0, 0.0);
   }
@@ -455,6 +478,7 @@ __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
 
   // 5) epilogue at the positions the inputs came from: fetch a group of
   //    operands, then finish it (one memory latency per group)
+  if (late_wait) pdl_wait();
   if (!active) return;
   constexpr int G = H < 4 ? H : 4;
 #pragma unroll
@@ -974,8 +998,7 @@ constexpr int paired_pts_for(bool ypass) {
 }
 template <int LOGM, class Pol>
 constexpr int paired_pts() { return paired_pts_for<LOGM>(std::is_same<Pol, YPass>::value); }
-__device__ __forceinline__ bool late_wait_of(const YPass&) { return false; }
-__device__ __forceinline__ bool late_wait_of(const XPass& p) { return p.late_wait != 0; }
+
 template <int LOGM, class Pol, int EPI>
 #ifndef FDE_PAIRED_CTAS
 #define FDE_PAIRED_CTAS 4  // resident 128-thread CTAs per SM the register budget is cut for
@@ -983,14 +1006,7 @@ template <int LOGM, class Pol, int EPI>
 __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CTA_THREADS,
                                   FDE_PAIRED_CTAS * 128 / PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CTA_THREADS)
     fft_line_kernel_paired(const Pol p) {
-  // Row pass behind a column pass that holds every tensor-memory column of
-  // every SM (p.late_wait, see launch_paired_epi): nothing before the
-  // epilogue depends on the column pass, so the wait for it moves there and
-  // this grid's first lines run in the slots the column pass's early
-  // finishers leave (2047 lines on 592 slots: the last round is half empty).
-  pdl_launch_dependents();
-  const bool late_wait = late_wait_of(p);
-  if (!late_wait) pdl_wait();
+  const bool late_wait = pass_enter(p);
   constexpr int P = paired_pts<LOGM, Pol>();
   using S = PairedShape<LOGM, P>;
   using IO = LineIO<Pol, EPI>;
@@ -1252,7 +1268,7 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CT
 // this is what the coarse multigrid levels run.
 template <class P>
 __global__ void __launch_bounds__(256) direct_line_kernel(const P p) {
-  pdl_enter();
+  if (pass_enter(p)) pdl_wait();  // (short lines: no late wait)
   constexpr int E = kDirectMax / 32;
   __shared__ double s_col[kDirectMax], s_row[kDirectMax];
   const int n = p.blk.n;
@@ -1373,7 +1389,7 @@ bool launch_fft(const P& p, cudaStream_t s) {
   const size_t smem = size_t(lpb) * 2 * S::BUF * sizeof(double);
   launch_k(fft_line_kernel<LOGM, P>, grid, S::T * lpb, smem, s, p);
   FDE_LAUNCH_CHECK();
-  return false;
+  return true;
 }
 
 #ifndef FDE_PAIRED
@@ -1411,9 +1427,6 @@ inline int paired_parity(const YPass& p) {
   return common_parity({p.x, p.epT, p.emT, p.qT ? p.q : nullptr});
 }
 
-// Returns true when the grid holds all 512 tensor-memory columns of every SM
-// until its first CTA exits: a paired kernel launched behind it cannot
-// allocate its own columns -- the first thing it does -- before then.
 template <int LOGM, class P, int EPI>
 bool launch_paired_epi(const P& p, cudaStream_t s) {
   constexpr int PP = paired_pts<LOGM, P>();
@@ -1424,8 +1437,8 @@ bool launch_paired_epi(const P& p, cudaStream_t s) {
   // the TMEM allocation).  What the carveout leaves of the SM's 256 KB is
   // L1: it keeps the spectral constants (64 KB per block at M = 2048) and
   // the twiddle tables resident across lines.
-  static DeviceCache<std::pair<int, bool>> resident;
-  const std::pair<int, bool> res = resident.get([](int dev) {
+  static DeviceCache<int> resident;
+  const int max_ctas = resident.get([](int dev) {
     int sms = 0, smem_sm = 0, smem_rsv = 0, regs_sm = 0;
     FDE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     FDE_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
@@ -1447,15 +1460,14 @@ bool launch_paired_epi(const P& p, cudaStream_t s) {
     if (carve > 100) carve = 100;
     FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
                                   cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-    return std::make_pair(sms * per_sm, per_sm * S::TCOLS_CTA == 512);
+    return sms * per_sm;
   });
-  const int max_ctas = res.first;
   const int groups = (lines_of(p) + S::LPC - 1) / S::LPC;
   const int ctas = (groups + S::NG - 1) / S::NG;
   launch_k(fft_line_kernel_paired<LOGM, P, EPI>, ctas < max_ctas ? ctas : max_ctas,
            S::CTA_THREADS, S::SMEM, s, p);
   FDE_LAUNCH_CHECK();
-  return ctas >= max_ctas && res.second;
+  return true;
 }
 
 template <int LOGM, class P>
@@ -1484,7 +1496,7 @@ bool launch_any(const P& p, cudaStream_t s) {
     case 0:
       launch_k(direct_line_kernel<P>, (lines + 7) / 8, 256, 0, s, p);
       FDE_LAUNCH_CHECK();
-      return false;
+      return true;
     case 6: return launch_fft<6>(p, s);
     case 7: return launch_fft<7>(p, s);
     case 8: return FDE_PAIRED8 ? launch_paired<8>(p, s) : launch_fft<8>(p, s);

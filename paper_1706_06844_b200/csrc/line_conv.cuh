@@ -148,12 +148,14 @@ struct XPass {
   double src_scale;
   int par = 0;         // set by the launcher: common base-address parity (line_conv.cu)
   int scratch_q = 0;   // q is library scratch read once: its L2 lines are discarded after the read
-  // the launch right before this one was the column pass that writes q and it
-  // reported a saturated grid (launch_line_pass): wait for it in the epilogue
+  // the launch right before this one was the column pass that writes q (it
+  // releases its dependents only after its own wait, line_conv.cu pass_enter):
+  // this pass waits for it in its first epilogue
   int late_wait = 0;
   __device__ __forceinline__ int nlines() const { return n2; }
   __device__ __forceinline__ double load(int line, int pos) const {
-    return x[(size_t)line * n1 + pos];
+    // before a late wait: through L2 (this SM's L1 may hold the buffer's older contents)
+    return late_wait ? __ldcg(x + (size_t)line * n1 + pos) : x[(size_t)line * n1 + pos];
   }
   __device__ __forceinline__ void prefetch(int line, int chunk) const {
     const size_t p = (size_t)line * n1 + (size_t)chunk * 16;
@@ -198,8 +200,8 @@ struct XPass {
   }
 };
 
-// true: the grid keeps every SM's tensor memory allocated until its first CTA
-// exits (what XPass::late_wait needs from the launch before it)
+// true: a kernel was launched (every column-pass kernel follows the protocol
+// XPass::late_wait needs from the launch before it)
 bool launch_line_pass(const YPass& p, cudaStream_t s);
 // out[i * n2 + j] = in[i + j * n1] (tiled through shared memory)
 void launch_transpose(const double* in, double* out, int n1, int n2, cudaStream_t s);

@@ -392,6 +392,14 @@ struct Fft {
 #ifndef FDE_MINB_BIG
 #define FDE_MINB_BIG 2
 #endif
+// resident CTAs the plain FFT kernels are compiled for: 4 (128 registers)
+// lets a 511- / 255-line level sit in one wave (V-cycle cfg4 627.5 -> 622.6 us)
+#ifndef FDE_MINB_9
+#define FDE_MINB_9 4
+#endif
+#ifndef FDE_MINB_SMALL
+#define FDE_MINB_SMALL 4
+#endif
 #ifndef FDE_MINB_P8
 #define FDE_MINB_P8 2
 #endif
@@ -407,7 +415,7 @@ struct FftShape {
   static constexpr int BUF = M + (T < 16 ? T : 0);     // per-buffer stride (doubles)
   static constexpr size_t SMEM = size_t(LPB) * 2 * BUF * sizeof(double);
   static constexpr int MINB = THREADS >= 256 ? (P == 8 && THREADS == 256 ? FDE_MINB_P8 : 1)
-                                             : (LOGM == 9 ? 2 : (LOGM >= 10 ? FDE_MINB_BIG : 3));
+                                             : (LOGM == 9 ? FDE_MINB_9 : (LOGM >= 10 ? FDE_MINB_BIG : FDE_MINB_SMALL));
 };
 
 // One CTA convolves LPB lines of length n <= M with T_b and T_b^T.

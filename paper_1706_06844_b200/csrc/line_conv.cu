@@ -845,6 +845,9 @@ constexpr int partner_slot(int s, bool t0) {
 // aligned in all streams -- bulk copies, 128-bit loads and 128-bit stores
 // apply to odd lines too (n + 1 <= M is checked by the host).
 // Pointers below address virtual position 0 (= element -sx).
+#ifndef FDE_EPI_G_Y
+#define FDE_EPI_G_Y 4  // 8 (every em pair of the line in flight at once): measured no change
+#endif
 #ifndef FDE_L2_STREAM
 #define FDE_L2_STREAM 1  // evict_first hints on the coefficient streams
 #endif
@@ -881,7 +884,7 @@ struct LineIO;
 template <int EPI>
 struct LineIO<YPass, EPI> {
   static constexpr bool QT = (EPI >> 1) & 1;
-  static constexpr int G = 4;  // slots per epilogue group
+  static constexpr int G = FDE_EPI_G_Y;  // slots per epilogue group 
   const double* x;
   const double* ep;
   const double* em;
@@ -1268,7 +1271,7 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CT
     //    group's are issued before the wait for the staged streams.
     {
       const IO io(p, line, sx);
-      constexpr int G = IO::G;
+      constexpr int G = IO::G < H ? IO::G : H;
       typename IO::Glob gl[G];
       auto fetch_group = [&](int g) {
 #pragma unroll
@@ -1282,14 +1285,12 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CT
         double2 ty[4];
         tmem_ld4(tqy + 4 * g4, ty);
 #pragma unroll
-        for (int g = g4; g < g4 + 4; g += G) {
-          if (g > 0) fetch_group(g);
-#pragma unroll
-          for (int c = 0; c < G; ++c) {
-            const int pv = 2 * (tl + (g + c) * T);
-            const double2 a = *reinterpret_cast<const double2*>(smem + pv);
-            io.finish(pv, live, ty[g - g4 + c], v[g + c], a, gl[c]);
-          }
+        for (int c4 = 0; c4 < 4; ++c4) {
+          const int slot = g4 + c4;
+          if (slot > 0 && slot % G == 0) fetch_group(slot);
+          const int pv = 2 * (tl + slot * T);
+          const double2 a = *reinterpret_cast<const double2*>(smem + pv);
+          io.finish(pv, live, ty[c4], v[slot], a, gl[slot % G]);
         }
       }
     }

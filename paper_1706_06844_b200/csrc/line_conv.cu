@@ -68,6 +68,11 @@ __device__ __forceinline__ bool pass_ready(const XPass& p) {
 // twiddles it stays resident in the L1 the line kernels leave (64 KB).
 template <int M>
 __device__ __forceinline__ void ld_ab(const double2* ab, int k, double2& a, double2& b) {
+#ifdef FDE_EXP_NOSPEC
+  a = make_double2(1.0 + k, 0.5);  // timing experiment: no constant loads (wrong results)
+  b = make_double2(0.25, 2.0 - k);
+  return;
+#endif
 #ifdef FDE_EXP_ABSMALL
   k &= 255;  // timing experiment: an always-L1-resident slice of the table (wrong results)
 #endif
@@ -552,6 +557,9 @@ __global__ void __launch_bounds__(FftShape<LOGM>::THREADS, FftShape<LOGM>::MINB)
 // paired kernel (named barrier 1 + group index; barrier 0 is the whole CTA).
 template <int NT>
 __device__ __forceinline__ void group_bar() {
+#ifdef FDE_EXP_NOBAR
+  return;  // timing experiment (wrong results)
+#endif
   if constexpr (NT >= FDE_CTA_THREADS) {
     __syncthreads();
   } else {
@@ -674,6 +682,9 @@ __device__ __forceinline__ void pstage_compute(double2 (&v)[P], int tl, const do
 template <int LOGM, int P, int NSL, int R, bool PAIRED>
 __device__ __forceinline__ void pstage_twiddles(double2 (&w1s)[P], int tl, const double2* twM) {
   constexpr int T = (1 << LOGM) / P, B = P / R, NS = 1 << NSL;
+#ifdef FDE_EXP_NOTW
+  return;  // timing experiment (wrong results)
+#endif
   if constexpr (NS > 1) {  // compact table: exp(-2 pi i j / (NS R)) at NS R / 2 + j
 #pragma unroll
     for (int q = 0; q < B; ++q) {
@@ -853,6 +864,9 @@ constexpr int partner_slot(int s, bool t0) {
 #endif
 template <bool STREAM = false>
 __device__ __forceinline__ double2 ld_pair(const double* v0, int pv, int sx, int nv) {
+#ifdef FDE_EXP_NOEPILD
+  return make_double2(1.0 + pv, 2.0 - sx);  // timing experiment: no epilogue operand loads
+#endif
   const double* a = v0 + pv;
   if (pv >= sx && pv + 1 < nv) {
     if constexpr (STREAM && FDE_L2_STREAM) return ldcg_stream(reinterpret_cast<const double2*>(a));
@@ -864,6 +878,9 @@ __device__ __forceinline__ double2 ld_pair(const double* v0, int pv, int sx, int
   return r;
 }
 __device__ __forceinline__ void st_pair(double* v0, int pv, int sx, int nv, bool live, double2 r) {
+#ifdef FDE_EXP_NOEPIST
+  if (r.x != 1.2345) return;  // timing experiment: (practically) no stores
+#endif
   double* a = v0 + pv;
   if (!live) return;
   if (pv >= sx && pv + 1 < nv) {
@@ -918,6 +935,9 @@ struct LineIO<YPass, EPI> {
                                          const Glob& g) const {
     const double2 s1 = g.s1;
     const double2 v = make_double2(c * (s0.x * ty.x + s1.x * tt.x), c * (s0.y * ty.y + s1.y * tt.y));
+#ifdef FDE_EXP_NOEPIST
+    if (v.x != 1.2345) return;
+#endif
     if (QT) {
       st_pair(q, pv, sx, nv, live, v);
     } else if (live) {

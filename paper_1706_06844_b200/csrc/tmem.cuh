@@ -33,6 +33,9 @@ __device__ __forceinline__ void tmem_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() {
+#ifdef FDE_EXP_NOTMEM
+  return;
+#endif
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() {
@@ -41,6 +44,9 @@ __device__ __forceinline__ void tmem_wait_ld() {
 
 // 4 complex doubles (16 columns) at column offset `taddr`
 __device__ __forceinline__ void tmem_st4(uint32_t taddr, const double2 (&v)[4]) {
+#ifdef FDE_EXP_NOTMEM
+  return;
+#endif
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
       "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
@@ -54,6 +60,9 @@ __device__ __forceinline__ void tmem_st4(uint32_t taddr, const double2 (&v)[4]) 
 }
 // 2 complex doubles (8 columns) at column offset `taddr`
 __device__ __forceinline__ void tmem_st2(uint32_t taddr, const double2 (&v)[2]) {
+#ifdef FDE_EXP_NOTMEM
+  return;
+#endif
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
       "r"(__double2loint(v[0].x)), "r"(__double2hiint(v[0].x)), "r"(__double2loint(v[0].y)),
@@ -63,6 +72,11 @@ __device__ __forceinline__ void tmem_st2(uint32_t taddr, const double2 (&v)[2]) 
 }
 // load + wait in one asm statement, so no consumer can be scheduled between
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, double2 (&v)[4]) {
+#ifdef FDE_EXP_NOTMEM
+#pragma unroll
+  for (int c = 0; c < 4; ++c) v[c] = make_double2(1.0 + taddr, 2.0 + c);
+  return;
+#endif
   int r[16];
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
@@ -81,6 +95,11 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, double2 (&v)[4]) {
 
 // 16 complex doubles (64 columns) in one load, one wait
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, double2 (&v)[16]) {
+#ifdef FDE_EXP_NOTMEM
+#pragma unroll
+  for (int c = 0; c < 16; ++c) v[c] = make_double2(v[c].x + taddr, v[c].y + c);
+  return;
+#endif
   int r[64];
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%64];\n\t"

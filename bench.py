@@ -206,7 +206,8 @@ def run_reference(args):
         "n_gpus": world, "steps": nsteps, "warmup": 0, "ms_per_step": 1e3 * wall / nsteps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded counter-hash U[0,1) source, SURVEY Appendix A)",
-        "config": dict(CONFIG, sample=f"{nsteps} real time step(s) m=1..{nsteps} of cfg4"),
+        "config": dict(CONFIG),  # the same dict in both arms; what this run sampled:
+        "sample": f"{nsteps} real time step(s) m=1..{nsteps} of cfg4",
         "iterations_per_step": [int(v) for v in r["its"]],
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind,
                          "sample": f"{nsteps} full reference time steps of cfg4 (assemble_rhs + "
@@ -465,7 +466,8 @@ def run_own(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded counter-hash U[0,1) source, SURVEY Appendix A)",
-        "config": dict(CONFIG, parallelism=("replica x%d" % world) if world > 1 else "single GPU"),
+        "config": dict(CONFIG),
+        "parallelism": ("replica x%d" % world) if world > 1 else "single GPU",
         "iterations_per_step": [int(v) for v in timed_its],
         "warmup_iterations": [int(v) for v in its],
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * N * N,
@@ -591,9 +593,10 @@ def run_own_distributed(args, prob, cfg, rank, world, local, dev, stream, barrie
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded counter-hash U[0,1) source, SURVEY Appendix A)",
-        "config": dict(CONFIG, parallelism=f"y-slab x{world} (C++ host, NCCL send/recv all-to-all "
-                                         f"transposes, rank-ordered all-gather dots, replicated "
-                                         f"coarse tail, graph-captured V-cycle)"),
+        "config": dict(CONFIG),
+        "parallelism": f"y-slab x{world} (C++ host, NCCL send/recv all-to-all transposes, "
+                       f"rank-ordered all-gather dots, replicated coarse tail, graph-captured "
+                       f"V-cycle)",
         "iterations_per_step": [int(v) for v in timed], "warmup_iterations": [int(v) for v in its],
         "gpu_launches": int(launches), "clocks": clocks,
         "collectives_per_step": collectives / max(total, 1),

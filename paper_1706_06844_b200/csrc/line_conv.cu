@@ -33,7 +33,9 @@ __device__ __forceinline__ int swz(int p) { return p ^ ((p >> SH) & 15); }
 // streams, through L2) was written by kernels BEFORE the column pass; the
 // column pass therefore lets its dependents launch only after its own wait,
 // i.e. once everything before it is complete and flushed.  Returns whether
-// the caller still owes the wait.
+// the caller still owes the wait.  (Doing the kernel's memory-free setup --
+// mbarriers, tensor-memory allocation -- before the wait measured slower:
+// 88.2 -> 83.0 steps/s.)
 __device__ __forceinline__ bool pass_enter(const YPass&) {
   pdl_wait();
   pdl_launch_dependents();
@@ -45,23 +47,6 @@ __device__ __forceinline__ bool pass_enter(const XPass& p) {
   pdl_wait();
   return false;
 }
-// The same in two steps for kernels with a memory-free prologue (barrier
-// initialisation, tensor-memory allocation), which then overlaps the tail of
-// the previous kernel: pass_open() first thing, pass_ready() before the first
-// global access.
-__device__ __forceinline__ void pass_open(const YPass&) {}
-__device__ __forceinline__ void pass_open(const XPass&) { pdl_launch_dependents(); }
-__device__ __forceinline__ bool pass_ready(const YPass&) {
-  pdl_wait();
-  pdl_launch_dependents();
-  return false;
-}
-__device__ __forceinline__ bool pass_ready(const XPass& p) {
-  if (p.late_wait) return true;
-  pdl_wait();
-  return false;
-}
-
 // Spectral constants of one k from the compact table (operator.cu): a_k at
 // index k (k < M), b_c at M + c for c <= M/2; b_k = b_k (k <= M/2) or
 // -conj(b_{M-k}).  48 KB per block at M = 2048: together with the stage
@@ -1047,9 +1032,6 @@ template <int LOGM, class Pol>
 constexpr int paired_pts() { return paired_pts_for<LOGM>(std::is_same<Pol, YPass>::value); }
 
 template <int LOGM, class Pol, int EPI>
-#ifndef FDE_PROLOGUE_FIRST
-#define FDE_PROLOGUE_FIRST 0  // barrier / tensor-memory setup before the wait for the previous kernel: measured 88.2 -> 83.0 steps/s
-#endif
 #ifndef FDE_STAGGER_Y_NS
 #define FDE_STAGGER_Y_NS 0
 #endif
@@ -1059,11 +1041,7 @@ template <int LOGM, class Pol, int EPI>
 __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CTA_THREADS,
                                   FDE_PAIRED_CTAS * 128 / PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CTA_THREADS)
     fft_line_kernel_paired(const Pol p) {
-#if FDE_PROLOGUE_FIRST
-  pass_open(p);
-#else
   const bool late_wait = pass_enter(p);
-#endif
   constexpr int P = paired_pts<LOGM, Pol>();
   using S = PairedShape<LOGM, P>;
   using IO = LineIO<Pol, EPI>;
@@ -1120,9 +1098,6 @@ __global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CT
   __syncthreads();
   tmem_fence_after();
   const uint32_t tbase = *s_tbase;
-#if FDE_PROLOGUE_FIRST
-  const bool late_wait = pass_ready(p);
-#endif
 #if FDE_STAGGER_Y_NS
   // experiment: groups with one line fewer than the longest start late (4 / 8 us: no gain)
   if (std::is_same<Pol, YPass>::value) {

@@ -11,13 +11,16 @@
 //    unpacked the same way on the way out), and spectrum(T^T) = conj
 //    spectrum(T) (c is real) so only one spectrum is stored, pre-scaled by
 //    1/(2L) so the whole pipeline runs unnormalised transforms.
-//  * FFTs are Stockham radix-8 (+ one radix-4/2 stage) with 8 points per
-//    thread held in registers; shared memory is only the exchange buffer
-//    between stages (SoA re/im, padded every 32 doubles against bank
-//    conflicts).  Twiddles are plain (non-__ldg) loads so ptxas cannot hoist
-//    them across the stage barriers (that blew the register budget).
-//  * Two passes per apply: the y-pass (columns, stride n1) runs first and
-//    writes Q = sign * s/r * (ep T_b x + em T_b^T x) using pre-transposed
+//  * FFTs are Stockham radix-16 stages (plus one radix-8/4/2 stage) with 16
+//    points per thread held in registers (8 or 4 on short lines); shared
+//    memory is only the exchange buffer between stages.  The two finest
+//    line lengths (M >= 1024) run the paired-spectrum kernel: Z[k] and
+//    Z[M-k] end in the same thread, the packed spectra are parked in tensor
+//    memory (tcgen05.st/ld), lines and coefficient streams arrive by bulk
+//    asynchronous copies, one persistent 128-thread CTA per line slot
+//    (line_conv.cu).
+//  * Two passes per apply: the y-pass (columns; of a transposed copy of x
+//    from 512 columns up) runs first and writes Q = sign * s/r * (ep T_b x + em T_b^T x) using pre-transposed
 //    ep/em; the x-pass (rows, contiguous) adds inv_r x + sign (dp T_a x +
 //    dm T_a^T x) + Q and applies a fused epilogue (plain store, rhs source
 //    add, residual b - Ax, damped-Jacobi update) -- all its streams coalesced.

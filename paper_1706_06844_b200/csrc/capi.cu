@@ -612,6 +612,7 @@ int fde_march_step(fde_march h, const double* source, int source_mode, void* str
                    size_t* iterations, double* residual) {
   return guard([&] {
     need(h != nullptr, "null handle");
+    NvtxRange trace("fde:time-step");
     cudaStream_t s = stream_of(stream);
     const size_t n = h->g.size();
     const size_t m = h->m + 1;

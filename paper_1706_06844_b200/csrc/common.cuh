@@ -1,6 +1,7 @@
 // Shared device/host helpers for the B200 CN-WSGD hot path.
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstdint>
@@ -37,6 +38,17 @@ extern std::atomic<unsigned long long> g_kernel_launches;
     ::fde_b200::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \
     ::fde_b200::cuda_check(cudaGetLastError(), "kernel launch");            \
   } while (0)
+
+// ---- tracing -------------------------------------------------------------
+// NVTX range over a host-side phase (time step, Krylov solve, V-cycle,
+// operator apply): shows up in Nsight timelines, a no-op without a tool
+// attached (header-only NVTX 3).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---- one-time per-device setup --------------------------------------------
 // Kernel attributes (opt-in shared memory, carveout) and occupancy-derived

@@ -195,6 +195,7 @@ double KrylovWorkspace::true_rel(const StructuredOp& a, const Precond* m, const 
 KrylovResult KrylovWorkspace::gmres(const StructuredOp& a, const Precond* m,
                                     const SolverConfig& cfg, const double* b, double* x_out,
                                     cudaStream_t s) {
+  NvtxRange trace("fde:gmres");
   const size_t n = n_;
   if (a.size() != n) throw InvalidArgument("rhs size mismatch");
   if (cfg.restart == 0 || !(cfg.tol > 0.0)) throw InvalidArgument("invalid solver configuration");
@@ -262,6 +263,7 @@ KrylovResult KrylovWorkspace::gmres(const StructuredOp& a, const Precond* m,
     bool enq[2] = {false, false}, chained[2] = {false, false};
     auto wbuf = [&](size_t i) { return (i & 1) ? w2_.get() : w_.get(); };
     auto enqueue = [&](size_t i) {
+      NvtxRange step_trace("fde:arnoldi-step");
       double* w = wbuf(i);
       a.apply(v_[i].get(), t_.get(), s);
       precondition(m, t_.get(), w, s);
@@ -369,6 +371,7 @@ KrylovResult KrylovWorkspace::gmres(const StructuredOp& a, const Precond* m,
 KrylovResult KrylovWorkspace::bicgstab(const StructuredOp& a, const Precond* m,
                                        const SolverConfig& cfg, const double* b, double* x,
                                        cudaStream_t s) {
+  NvtxRange trace("fde:bicgstab");
   const size_t n = n_;
   if (a.size() != n) throw InvalidArgument("rhs size mismatch");
   if (cfg.restart == 0 || cfg.max_outer == 0 || !(cfg.tol > 0.0))

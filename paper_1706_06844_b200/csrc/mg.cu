@@ -280,6 +280,7 @@ void Hierarchy::refactor_coarse(cudaStream_t s) {
 }
 
 void Hierarchy::vcycle(const double* b, double* x, bool zero_guess, cudaStream_t s) const {
+  NvtxRange trace("fde:vcycle");
   cycle(0, b, x, zero_guess, s);
 }
 

@@ -346,6 +346,7 @@ void StructuredOp::run_mapped(const InMap& in, double* x, double* out, double si
 
 void StructuredOp::run_impl(const InMap* in, const double* x, double* out, double sign, int epi,
                             const EpiArgs& e, cudaStream_t s) const {
+  NvtxRange trace("fde:apply");
   YPass yp{};
   yp.blk = ay_.dev();
   yp.n1 = (int)n1_;

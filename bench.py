@@ -331,7 +331,11 @@ def run_own(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # FDE_BENCH_FORCE_SLAB=1 (under torchrun with one rank): run the N > 1 code
+    # path -- y-slab march over NCCL -- at world size 1, the only way to
+    # exercise it where a single GPU is available
+    slab = world > 1 or os.environ.get("FDE_BENCH_FORCE_SLAB") == "1"
+    if slab:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     fde.load_library()
@@ -347,7 +351,7 @@ def run_own(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    if world > 1:
+    if slab:
         return run_own_distributed(args, prob, cfg, rank, world, local, dev, stream, barrier)
 
     # ---- value: sources resident in HBM

@@ -335,10 +335,15 @@ DistLevel::DistLevel(SlabComm& c, const Problem& p, size_t nf1, size_t nf2, size
 }
 
 void DistLevel::run(const double* x, double* out, double sign, int epi, const EpiArgs& e,
-                    cudaStream_t s) {
+                    cudaStream_t s, const InMap* in) {
   const PdlOff plain;
   const int P = comm.world();
-  if (nr) launch_transpose(x, xTl_.get(), (int)d1, (int)nr, s);  // [nr][d1] -> [d1][nr]
+  // [nr][d1] -> [d1][nr]; with an input map x = in(.) is formed (and stored)
+  // on the way, as StructuredOp::run_mapped does
+  if (nr && in)
+    launch_transpose_mapped(*in, const_cast<double*>(x), xTl_.get(), (int)d1, (int)nr, s);
+  else if (nr)
+    launch_transpose(x, xTl_.get(), (int)d1, (int)nr, s);
   comm.all_to_all(xTl_.get(), s1_.data(), recv_.get(), r1_.data(), s);
   block_permute(recv_.get(), xT_.get(), nc, d2, rows_ll_.data(), P, 0, s);  // -> [nc][d2]
   op_->ypass(xT_.get(), QT_.get(), sign, s);
@@ -532,11 +537,22 @@ void DistHierarchy::cycle(size_t l, const double* b, double* x, bool zero, cudaS
     }
     return;
   }
-  presmooth();
   double* r_local = r_[l].get() + halo_off(lv.d1);
   EpiArgs e;
   e.b = b;
-  lv.run(x, r_local, 1.0, EPI_RESID, e, s);  // r = b - A x
+  if (zero) {
+    // x = omega dinv b rides on the residual's local transpose (multigrid.cpp:355-356)
+    InMap zin{};
+    zin.kind = 1;
+    zin.a = b;
+    zin.d = lv.dinv.get();
+    zin.w = omega_;
+    zin.ld = (int)lv.d1;
+    lv.run(x, r_local, 1.0, EPI_RESID, e, s, &zin);  // x, r = b - A x
+  } else {
+    presmooth();
+    lv.run(x, r_local, 1.0, EPI_RESID, e, s);  // r = b - A x
+  }
   if (last_slab) {
     const int rk = comm_.rank(), P = comm_.world();
     const size_t k1 = dims_[l + 1].first;
@@ -635,13 +651,32 @@ DistGmres::~DistGmres() {
   if (hsc_) cudaFreeHost(hsc_);
 }
 
-void DistGmres::gdot(const double* x, const double* y, int slot, bool sqrt_out, cudaStream_t s) {
-  if (n_) red_.dot(n_, x, y, dpart_.get(), s, false);
-  else dpart_.zero(s);
+// this rank's partial in dpart_ -> the rank-ordered global sum in slot
+void DistGmres::gsum(int slot, bool sqrt_out, cudaStream_t s) {
   comm_.all_gather(dpart_.get(), dall_.get(), 1, s);
   launch_k(k_ordered_sum, 1, 32, 0, s, (const double*)dall_.get(), comm_.world(),
            dsc_.get() + slot, sqrt_out ? 1 : 0);
   FDE_LAUNCH_CHECK();
+}
+void DistGmres::gdot(const double* x, const double* y, int slot, bool sqrt_out, cudaStream_t s) {
+  if (n_) red_.dot(n_, x, y, dpart_.get(), s, false);
+  else dpart_.zero(s);
+  gsum(slot, sqrt_out, s);
+}
+// One modified Gram-Schmidt sweep over v_0 .. v_i with the coefficients in
+// slots base + 1 + k and the final norm in base + 2 + i (krylov.cpp:92-97):
+// each subtraction w -= h_k v_k is fused with the next projection <v_{k+1}, w>
+// (the last with ||w||^2) -- one pass over w per basis vector instead of two
+void DistGmres::gram_schmidt(size_t i, double* w, int base, cudaStream_t s) {
+  gdot(v_[0].get(), w, base + 1, false, s);
+  for (size_t k = 0; k <= i; ++k) {
+    if (n_)
+      red_.mgs(n_, w, v_[k].get(), dsc_.get() + base + 1 + k, k < i ? v_[k + 1].get() : w,
+               dpart_.get(), false, s);
+    else
+      dpart_.zero(s);
+    gsum(base + 2 + (int)k, k == i, s);
+  }
 }
 
 void DistGmres::fetch(int first, int count, cudaStream_t s) {
@@ -715,22 +750,14 @@ DistReport DistGmres::solve(const double* b, double* x, const SolverConfig& cfg,
       pc(t_.get(), w_.get(), s);
       double* w = w_.get();
       gdot(w, w, 0, true, s);  // ||w||
-      for (size_t k = 0; k <= i; ++k) {  // modified Gram-Schmidt, krylov.cpp:92-97
-        gdot(v_[k].get(), w, 1 + (int)k, false, s);
-        vec_axpy_dev(n_, dsc_.get() + 1 + k, -1.0, v_[k].get(), w, s);
-      }
-      gdot(w, w, 2 + (int)i, true, s);
+      gram_schmidt(i, w, 0, s);
       vec_scale_inv_dev(n_, dsc_.get() + 2 + i, w, v_[i + 1].get(), s);
       fetch(0, (int)i + 3, s);  // the step's one host read
       const double norm0 = hsc_[0];
       for (size_t k = 0; k <= i; ++k) h[i * ld + k] = hsc_[1 + k];
       double nrmw = hsc_[2 + i];
       if (nrmw < 1e-8 * norm0) {  // second pass, krylov.cpp:98-104
-        for (size_t k = 0; k <= i; ++k) {
-          gdot(v_[k].get(), w, blk + 1 + (int)k, false, s);
-          vec_axpy_dev(n_, dsc_.get() + blk + 1 + k, -1.0, v_[k].get(), w, s);
-        }
-        gdot(w, w, blk + 2 + (int)i, true, s);
+        gram_schmidt(i, w, blk, s);
         vec_scale_inv_dev(n_, dsc_.get() + blk + 2 + i, w, v_[i + 1].get(), s);
         fetch(blk, (int)i + 3, s);
         for (size_t k = 0; k <= i; ++k) h[i * ld + k] += hsc_[blk + 1 + k];

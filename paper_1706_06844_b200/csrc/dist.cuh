@@ -78,7 +78,8 @@ class DistLevel {
             std::vector<size_t> row_offsets, size_t steps, size_t m);
   size_t local_size() const { return nr * d1; }
   // out = epilogue(A x) on the rank's rows (SlabOp::xpass epilogues)
-  void run(const double* x, double* out, double sign, int epi, const EpiArgs& e, cudaStream_t s);
+  void run(const double* x, double* out, double sign, int epi, const EpiArgs& e,
+           cudaStream_t s, const InMap* in = nullptr);
   SlabComm& comm;
   size_t d1, d2, r0, r1, c0, c1, nr, nc;
   std::vector<size_t> rows, cols;
@@ -152,6 +153,8 @@ class DistGmres {
  private:
   // *slot = sum over ranks (rank order) of <x, y>, square-rooted if asked
   void gdot(const double* x, const double* y, int slot, bool sqrt_out, cudaStream_t s);
+  void gsum(int slot, bool sqrt_out, cudaStream_t s);
+  void gram_schmidt(size_t i, double* w, int base, cudaStream_t s);
   void fetch(int first, int count, cudaStream_t s);
   void pc(const double* r, double* z, cudaStream_t s);
   SlabComm& comm_;

@@ -1,5 +1,6 @@
 #include <cstdlib>
 #include "vec_kernels.cuh"
+#include "tmem.cuh"
 
 namespace fde_b200 {
 namespace {
@@ -513,6 +514,211 @@ __global__ void __launch_bounds__(kChainThreads, 1)
   }
 }
 
+// The same chain with w in TENSOR MEMORY and the current basis vector in shared
+// memory.  A pass of k_mgs_chain brings two slices per SM through L2 (v_{k+1}
+// from HBM, v_k again from L2) and measured 11 us with the grid barrier taken
+// out -- the L2 -> SM path, not HBM, bounds it.  Here the slice of v_{k+1} a
+// pass streams for its dot product is left in shared memory and is the v_k of
+// the next pass's subtraction, so a pass reads ONE vector slice through L2;
+// the CTA's slice of w (226 KB at n = 2047, the whole shared memory before)
+// lives in the SM's 256 KB of tensor memory instead: thread t of warp q owns
+// lane 32 (q % 4) + t % 32, columns 64 (q / 4) .. + 63, i.e. 16 double2 = the
+// pairs t + 1024 c (c < 16) of the slice.  Same per-element arithmetic, same
+// element -> thread map, same partial-sum order as k_mgs_chain: identical bits.
+constexpr int kChainSlots = 16;  // double2 per thread in tensor memory
+#ifndef FDE_CHAIN_LOADS
+#define FDE_CHAIN_LOADS 4  // 16-byte loads of v_{k+1} in flight per thread; 8 / 16 spill at 64 registers: 10.3 -> 13.1 / 14.5 us per pass
+#endif
+// (an L2 bulk prefetch of the next pass's slice measured +1.3 us per pass in
+// isolation and nothing in the step: left out)
+__global__ void __launch_bounds__(kChainThreads, 1)
+    k_mgs_chain_tmem(size_t n, size_t chunk, double* __restrict__ w,
+                     const double* const* __restrict__ v, int last, double* dh, double* dnorm0,
+                     double* dnrmw, double* __restrict__ vout, double* partials,
+                     unsigned int* bar) {
+  extern __shared__ __align__(16) double vs[];  // this CTA's slice of the pass's basis vector
+  __shared__ double red[2][kChainThreads / 32];
+  __shared__ double sums[2];
+  __shared__ uint32_t s_tbase;
+  __shared__ double w_tail;  // the odd last element of the last slice
+  const size_t lo = blockIdx.x * chunk;
+  const int cnt = lo < n ? (int)((n - lo < chunk) ? n - lo : chunk) : 0;
+  const uint64_t keep = policy_keep(), stream = policy_stream();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) tmem_alloc<512>(&s_tbase);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = s_tbase;
+  const uint32_t tw = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 64);
+  unsigned phase = 0;
+  auto grid_sum = [&](double a, double b) {
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) {
+      red[0][warp] = a;
+      red[1][warp] = b;
+    }
+    __syncthreads();
+    double* const part = partials + (phase & 1) * 2 * gridDim.x;
+    if (warp == 0) {  // the 32 warp partials, shuffle tree (fixed order)
+      const double ta = warp_sum(red[0][lane]), tb = warp_sum(red[1][lane]);
+      if (lane == 0) {
+        part[2 * blockIdx.x] = ta;
+        part[2 * blockIdx.x + 1] = tb;
+      }
+    }
+    ++phase;
+    grid_barrier(bar, phase * gridDim.x);
+    if (warp == 0) {
+      double ta = 0.0, tb = 0.0;
+      for (int k = lane; k < (int)gridDim.x; k += 32) {
+        ta += __ldcg(part + 2 * k);
+        tb += __ldcg(part + 2 * k + 1);
+      }
+      ta = warp_sum(ta);
+      tb = warp_sum(tb);
+      if (lane == 0) {
+        sums[0] = ta;
+        sums[1] = tb;
+      }
+    }
+    __syncthreads();
+  };
+  double2* const vs2 = reinterpret_cast<double2*>(vs);
+  const int pairs = cnt >> 1, tail = (cnt & 1) ? cnt - 1 : -1;
+  // ||w|| and <w, v_0>: w moves into tensor memory, v_0 into shared memory
+  {
+    const double* v0 = v[0] + lo;
+    const double* wg = w + lo;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int g = 0; g < kChainSlots; g += 4) {
+      double2 wv[4], vv[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int e = threadIdx.x + (g + c) * kChainThreads;
+        wv[c] = e < pairs ? ld2_hint(wg + 2 * e, stream) : make_double2(0.0, 0.0);
+        vv[c] = e < pairs ? ld2_hint(v0 + 2 * e, keep) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int e = threadIdx.x + (g + c) * kChainThreads;
+        if (e < pairs) {
+          vs2[e] = vv[c];
+          a0 = fma(wv[c].x, wv[c].x, a0);
+          a1 = fma(vv[c].x, wv[c].x, a1);
+          a0 = fma(wv[c].y, wv[c].y, a0);
+          a1 = fma(vv[c].y, wv[c].y, a1);
+        }
+      }
+      tmem_st4(tw + 4 * g, wv);
+    }
+    if (threadIdx.x == 0 && tail >= 0) {
+      const double wi = wg[tail];
+      w_tail = wi;
+      a0 = fma(wi, wi, a0);
+      a1 = fma(v0[tail], wi, a1);
+    }
+    tmem_wait_st();
+    grid_sum(a0, a1);
+  }
+  const double norm0 = sqrt(sums[0]);
+  double h = sums[1];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *dnorm0 = norm0;
+    dh[0] = h;
+  }
+  double hip = 0.0;
+  // w -= h_k v_k (v_k from shared memory) fused with <v_{k+1}, w> (v_{k+1}
+  // streamed once, left in shared memory for the next pass); the last pass
+  // forms ||w||
+  for (int k = 0; k <= last; ++k) {
+    const double* vk = v[k] + lo;
+    const double* vn = k < last ? v[k + 1] + lo : nullptr;
+    const double nh = -h;
+    double acc = 0.0;
+    __syncthreads();  // sums[] is rewritten by this pass's reduction
+#pragma unroll
+    for (int g8 = 0; g8 < kChainSlots; g8 += FDE_CHAIN_LOADS) {
+      // FDE_CHAIN_LOADS slices of v_{k+1} in flight per thread, then tensor
+      // memory in groups of 4 slots
+      double2 nv[FDE_CHAIN_LOADS];
+      if (vn) {
+#pragma unroll
+        for (int c = 0; c < FDE_CHAIN_LOADS; ++c) {
+          const int e = threadIdx.x + (g8 + c) * kChainThreads;
+          nv[c] = e < pairs ? ld2_hint(vn + 2 * e, keep) : make_double2(0.0, 0.0);
+        }
+      }
+#pragma unroll
+      for (int g = g8; g < g8 + FDE_CHAIN_LOADS; g += 4) {
+        double2 wv[4];
+        tmem_ld4(tw + 4 * g, wv);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int e = threadIdx.x + (g + c) * kChainThreads;
+          if (e < pairs) {
+            const double2 a = vs2[e];
+            double2 wi = wv[c];
+            wi.x = fma(nh, a.x, wi.x);
+            wi.y = fma(nh, a.y, wi.y);
+            wv[c] = wi;
+            if (vn) {
+              acc = fma(nv[g - g8 + c].x, wi.x, acc);
+              acc = fma(nv[g - g8 + c].y, wi.y, acc);
+              vs2[e] = nv[g - g8 + c];
+            } else {
+              acc = fma(wi.x, wi.x, acc);
+              acc = fma(wi.y, wi.y, acc);
+            }
+          }
+        }
+        tmem_st4(tw + 4 * g, wv);
+      }
+    }
+    if (threadIdx.x == 0 && tail >= 0) {
+      const double wi = fma(nh, vk[tail], w_tail);
+      w_tail = wi;
+      acc = fma(vn ? vn[tail] : wi, wi, acc);
+    }
+    tmem_wait_st();
+    grid_sum(acc, 0.0);
+    if (k < last) {
+      h = sums[0];
+      if (blockIdx.x == 0 && threadIdx.x == 0) dh[k + 1] = h;
+    } else {
+      hip = sqrt(sums[0]);
+      if (blockIdx.x == 0 && threadIdx.x == 0) *dnrmw = hip;
+    }
+  }
+  // v_{i+1} = w (1 / ||w||) (copy_scale, krylov.cpp:127-130); a second
+  // Gram-Schmidt pass (hip < 1e-8 norm0, krylov.cpp:98-104) needs w itself
+  const bool keep_w = hip < 1e-8 * norm0;
+  const double a = keep_w ? 1.0 : 1.0 / hip;
+  double2* const out2 = reinterpret_cast<double2*>((keep_w ? w : vout) + lo);
+#pragma unroll
+  for (int g = 0; g < kChainSlots; g += 4) {
+    double2 wv[4];
+    tmem_ld4(tw + 4 * g, wv);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int e = threadIdx.x + (g + c) * kChainThreads;
+      if (e < pairs) out2[e] = keep_w ? wv[c] : make_double2(wv[c].x * a, wv[c].y * a);
+    }
+  }
+  if (threadIdx.x == 0 && tail >= 0) (keep_w ? w : vout)[lo + tail] = keep_w ? w_tail : w_tail * a;
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tbase);
+}
+
+
+#ifndef FDE_CHAIN_TMEM
+#define FDE_CHAIN_TMEM 1  // w in tensor memory, one basis-vector slice per pass through L2
+#endif
+constexpr auto kChainKernel = FDE_CHAIN_TMEM ? k_mgs_chain_tmem : k_mgs_chain;
+
 struct RankOffsets {
   long long o[65];
   int n;
@@ -654,9 +860,9 @@ bool Reducer::mgs_chain(size_t n, double* w, const double* const* v_dev, int las
       if (e[0] == '0') coop = 0;
     if (coop) {
       cudaFuncAttributes fa{};
-      FDE_CUDA(cudaFuncGetAttributes(&fa, k_mgs_chain));
+      FDE_CUDA(cudaFuncGetAttributes(&fa, kChainKernel));
       r.max_smem = (size_t)optin - fa.sharedSizeBytes;
-      FDE_CUDA(cudaFuncSetAttribute(k_mgs_chain, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      FDE_CUDA(cudaFuncSetAttribute(kChainKernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)r.max_smem));
       r.grid = sms;
     }
@@ -667,6 +873,7 @@ bool Reducer::mgs_chain(size_t n, double* w, const double* const* v_dev, int las
   if (grid == 0) return false;
   const size_t chunk = ((n + grid - 1) / grid + 1) & ~size_t(1);
   if (chunk * sizeof(double) > max_smem) return false;
+  if (FDE_CHAIN_TMEM && chunk > 2 * (size_t)kChainSlots * kChainThreads) return false;
   if (chain_partials_.size() == 0) {
     chain_partials_.alloc(4 * (size_t)grid);
     chain_bar_.alloc(1);
@@ -682,7 +889,7 @@ bool Reducer::mgs_chain(size_t n, double* w, const double* const* v_dev, int las
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cuda_check(cudaLaunchKernelEx(&cfg, k_mgs_chain, n, chunk, w, v_dev, last, dh, dnorm0, dnrmw,
+  cuda_check(cudaLaunchKernelEx(&cfg, kChainKernel, n, chunk, w, v_dev, last, dh, dnorm0, dnrmw,
                                 vout, chain_partials_.get(), chain_bar_.get()),
              "kernel launch");
   FDE_LAUNCH_CHECK();

@@ -717,7 +717,12 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 #ifndef FDE_CHAIN_TMEM
 #define FDE_CHAIN_TMEM 1  // w in tensor memory, one basis-vector slice per pass through L2
 #endif
-constexpr auto kChainKernel = FDE_CHAIN_TMEM ? k_mgs_chain_tmem : k_mgs_chain;
+// slices from this many doubles per SM up run the tensor-memory chain; below,
+// the allocation and the fixed 16-slot walk cost more than the second L2
+// stream (cfg1 894 -> 808, cfg2 650 -> 611 steps/s with it)
+#ifndef FDE_CHAIN_TMEM_MIN
+#define FDE_CHAIN_TMEM_MIN 4096
+#endif
 
 struct RankOffsets {
   long long o[65];
@@ -859,11 +864,16 @@ bool Reducer::mgs_chain(size_t n, double* w, const double* const* v_dev, int las
     if (const char* e = std::getenv("FDE_MGS_CHAIN"))
       if (e[0] == '0') coop = 0;
     if (coop) {
-      cudaFuncAttributes fa{};
-      FDE_CUDA(cudaFuncGetAttributes(&fa, kChainKernel));
-      r.max_smem = (size_t)optin - fa.sharedSizeBytes;
-      FDE_CUDA(cudaFuncSetAttribute(kChainKernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)r.max_smem));
+      size_t room = (size_t)optin;
+      for (auto kern : {k_mgs_chain, k_mgs_chain_tmem}) {
+        cudaFuncAttributes fa{};
+        FDE_CUDA(cudaFuncGetAttributes(&fa, kern));
+        if ((size_t)optin - fa.sharedSizeBytes < room) room = (size_t)optin - fa.sharedSizeBytes;
+      }
+      r.max_smem = room;
+      for (auto kern : {k_mgs_chain, k_mgs_chain_tmem})
+        FDE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)r.max_smem));
       r.grid = sms;
     }
     return r;
@@ -873,7 +883,8 @@ bool Reducer::mgs_chain(size_t n, double* w, const double* const* v_dev, int las
   if (grid == 0) return false;
   const size_t chunk = ((n + grid - 1) / grid + 1) & ~size_t(1);
   if (chunk * sizeof(double) > max_smem) return false;
-  if (FDE_CHAIN_TMEM && chunk > 2 * (size_t)kChainSlots * kChainThreads) return false;
+  const bool in_tmem = FDE_CHAIN_TMEM && chunk >= FDE_CHAIN_TMEM_MIN &&
+                       chunk <= 2 * (size_t)kChainSlots * kChainThreads;
   if (chain_partials_.size() == 0) {
     chain_partials_.alloc(4 * (size_t)grid);
     chain_bar_.alloc(1);
@@ -889,7 +900,8 @@ bool Reducer::mgs_chain(size_t n, double* w, const double* const* v_dev, int las
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cuda_check(cudaLaunchKernelEx(&cfg, kChainKernel, n, chunk, w, v_dev, last, dh, dnorm0, dnrmw,
+  cuda_check(cudaLaunchKernelEx(&cfg, in_tmem ? k_mgs_chain_tmem : k_mgs_chain, n, chunk, w, v_dev,
+                                last, dh, dnorm0, dnrmw,
                                 vout, chain_partials_.get(), chain_bar_.get()),
              "kernel launch");
   FDE_LAUNCH_CHECK();

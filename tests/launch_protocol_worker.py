@@ -37,4 +37,14 @@ for cfg in (4, 2, 1):
         mg.vcycle(b, x, zero_guess=True)
         b = x / x.abs().max()
     h.update(b.cpu().numpy().tobytes())
+# whole time steps (GMRES + V-cycle + the one-launch Gram-Schmidt): iteration counts and solutions
+for cfg, steps in ((2, 8), (4, 3)):
+    p = fde.Problem.preset_config(cfg, steps=steps)
+    dc = fde.DriverConfig(precond=fde.PRECOND_MGM, tol=1e-8, restart=20, max_outer=100, omega=0.7,
+                          cycles=1, coarse=fde.COARSE_SWEEPS, coarse_sweeps=3)
+    m = fde.March(p, p.n, p.n, steps, dc)
+    for _ in range(steps):
+        it, res = m.step()
+        h.update(str(it).encode())
+    h.update(m.solution().tobytes())
 print("DIGEST", h.hexdigest())

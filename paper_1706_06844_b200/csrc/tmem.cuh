@@ -236,6 +236,22 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc, int 
                "l"(gsrc), "r"(src_bytes)
                : "memory");
 }
+// 16-byte copy past L1 with an L2 eviction-priority hint
+__device__ __forceinline__ void cp_async16_hint(void* smem_dst, const void* gsrc, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(
+                   smem_addr_u32(smem_dst)),
+               "l"(gsrc), "l"(pol)
+               : "memory");
+}
+// at most n (0..3) of this thread's committed groups still pending
+__device__ __forceinline__ void cp_async_wait_group_le(int n) {
+  switch (n) {
+    case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+  }
+}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
 }

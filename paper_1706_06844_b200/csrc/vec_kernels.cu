@@ -526,6 +526,9 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 // pairs t + 1024 c (c < 16) of the slice.  Same per-element arithmetic, same
 // element -> thread map, same partial-sum order as k_mgs_chain: identical bits.
 constexpr int kChainSlots = 16;  // double2 per thread in tensor memory
+#ifndef FDE_CHAIN_ASYNC
+#define FDE_CHAIN_ASYNC 1  // v_{k+1} by per-thread asynchronous copies into its shared-memory slots
+#endif
 #ifndef FDE_CHAIN_LOADS
 #define FDE_CHAIN_LOADS 4  // 16-byte loads of v_{k+1} in flight per thread; 8 / 16 spill at 64 registers: 10.3 -> 13.1 / 14.5 us per pass
 #endif
@@ -592,6 +595,50 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     const double* v0 = v[0] + lo;
     const double* wg = w + lo;
     double a0 = 0.0, a1 = 0.0;
+#if FDE_CHAIN_ASYNC
+    // v_0 straight into its shared-memory slots (no registers), w through
+    // registers into tensor memory; <w, v_0> in a second walk, slot order
+#pragma unroll
+    for (int g = 0; g < kChainSlots; g += 4) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int e = threadIdx.x + (g + c) * kChainThreads;
+        if (e < pairs) cp_async16_hint(vs2 + e, v0 + 2 * e, keep);
+      }
+      cp_async_commit();
+    }
+#pragma unroll 1  // (unrolled, the loads of every round are hoisted and spill)
+    for (int g = 0; g < kChainSlots; g += 4) {
+      double2 wv[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int e = threadIdx.x + (g + c) * kChainThreads;
+        wv[c] = e < pairs ? ld2_hint(wg + 2 * e, stream) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {  // (zero beyond the slice: adds +0.0)
+        a0 = fma(wv[c].x, wv[c].x, a0);
+        a0 = fma(wv[c].y, wv[c].y, a0);
+      }
+      tmem_st4(tw + 4 * g, wv);
+    }
+    tmem_wait_st();
+#pragma unroll
+    for (int g = 0; g < kChainSlots; g += 4) {
+      cp_async_wait_group_le(3 - g / 4);
+      double2 wv[4];
+      tmem_ld4(tw + 4 * g, wv);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int e = threadIdx.x + (g + c) * kChainThreads;
+        if (e < pairs) {
+          const double2 b = vs2[e];
+          a1 = fma(b.x, wv[c].x, a1);
+          a1 = fma(b.y, wv[c].y, a1);
+        }
+      }
+    }
+#else
 #pragma unroll
     for (int g = 0; g < kChainSlots; g += 4) {
       double2 wv[4], vv[4];
@@ -614,6 +661,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
       }
       tmem_st4(tw + 4 * g, wv);
     }
+#endif
     if (threadIdx.x == 0 && tail >= 0) {
       const double wi = wg[tail];
       w_tail = wi;
@@ -639,6 +687,61 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     const double nh = -h;
     double acc = 0.0;
     __syncthreads();  // sums[] is rewritten by this pass's reduction
+#if FDE_CHAIN_ASYNC
+    // Every pair of the slice belongs to one thread (shared-memory slot and
+    // tensor-memory slot alike), so the thread that has subtracted h_k v_k[e]
+    // can overwrite its slot with v_{k+1}[e] by an asynchronous copy: all 16
+    // loads of a thread are in flight at once and hold no register.  The dot
+    // product follows in a second walk (w once more from tensor memory), in
+    // the same slot order as the fused walk: identical bits.
+#pragma unroll
+    for (int g = 0; g < kChainSlots; g += 4) {
+      double2 wv[4];
+      tmem_ld4(tw + 4 * g, wv);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int e = threadIdx.x + (g + c) * kChainThreads;
+        if (e < pairs) {
+          const double2 a = vs2[e];
+          double2 wi = wv[c];
+          wi.x = fma(nh, a.x, wi.x);
+          wi.y = fma(nh, a.y, wi.y);
+          wv[c] = wi;
+          if (!vn) {
+            acc = fma(wi.x, wi.x, acc);
+            acc = fma(wi.y, wi.y, acc);
+          }
+        }
+      }
+      tmem_st4(tw + 4 * g, wv);  // (depends on every vs2[e] read of the group)
+      if (vn) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int e = threadIdx.x + (g + c) * kChainThreads;
+          if (e < pairs) cp_async16_hint(vs2 + e, vn + 2 * e, keep);
+        }
+        cp_async_commit();
+      }
+    }
+    if (vn) {
+      tmem_wait_st();
+#pragma unroll
+      for (int g = 0; g < kChainSlots; g += 4) {
+        cp_async_wait_group_le(3 - g / 4);
+        double2 wv[4];
+        tmem_ld4(tw + 4 * g, wv);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int e = threadIdx.x + (g + c) * kChainThreads;
+          if (e < pairs) {
+            const double2 b = vs2[e];
+            acc = fma(b.x, wv[c].x, acc);
+            acc = fma(b.y, wv[c].y, acc);
+          }
+        }
+      }
+    }
+#else
 #pragma unroll
     for (int g8 = 0; g8 < kChainSlots; g8 += FDE_CHAIN_LOADS) {
       // FDE_CHAIN_LOADS slices of v_{k+1} in flight per thread, then tensor
@@ -677,6 +780,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
         tmem_st4(tw + 4 * g, wv);
       }
     }
+#endif
     if (threadIdx.x == 0 && tail >= 0) {
       const double wi = fma(nh, vk[tail], w_tail);
       w_tail = wi;

@@ -356,70 +356,85 @@ __global__ void k_prolong(Xfer t, const double* __restrict__ c, int c_lo,
 // (deterministic, identical in every CTA).
 constexpr int kChainThreads = 1024;
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// all CTAs of the (co-resident) grid reach the barrier; *bar counts arrivals.
-// The arrival is a release (orders this CTA's partials before it), the
-// polling load an acquire: no full fences on the critical path.
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-    while (ld_acquire_u32(bar) < target) __nanosleep(32);
+// Grid-wide sums of (a, b) without atomics: every CTA publishes its two
+// partial sums as four 8-byte words {32 bits of the double, 32-bit epoch}
+// (an aligned 8-byte access is single-copy atomic, so a word carries its own
+// "valid" flag and no fence or counter is needed -- the data IS the flag),
+// and thread k of every CTA polls CTA k's words until they carry this epoch:
+// one L2 round trip per reduction instead of three (arrive, poll, read the
+// partials).  Slots are double-buffered by epoch parity: a CTA can run at
+// most one reduction ahead of the slowest reader.  Every warp then adds the
+// gathered partials in CTA order (lane-strided, shuffle tree) exactly as
+// the counter version did: identical bits, identical in every CTA.
+constexpr int kChainMaxGrid = 160;  // CTAs (one per SM); 2.5 KB of gather slots
+struct ChainShared {
+  double red[2][kChainThreads / 32];
+  double gath[2][kChainMaxGrid];
+};
+__device__ __forceinline__ double2 chain_grid_sum(double a, double b, ChainShared& sh,
+                                                  unsigned long long* ll, unsigned& phase) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grid = (int)gridDim.x;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (lane == 0) {
+    sh.red[0][warp] = a;
+    sh.red[1][warp] = b;
   }
   __syncthreads();
+  ++phase;
+  unsigned long long* const slots = ll + (size_t)(phase & 1) * 4 * grid;
+  if (warp == 0) {  // the 32 warp partials, shuffle tree (fixed order)
+    double ta = warp_sum(sh.red[0][lane]), tb = warp_sum(sh.red[1][lane]);
+    ta = __shfl_sync(0xffffffffu, ta, 0);
+    tb = __shfl_sync(0xffffffffu, tb, 0);
+    if (lane < 4) {
+      const double val = lane < 2 ? ta : tb;
+      const unsigned half = (lane & 1) ? (unsigned)__double2hiint(val) : (unsigned)__double2loint(val);
+      const unsigned long long word = ((unsigned long long)phase << 32) | half;
+      asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(slots + 4 * blockIdx.x + lane),
+                   "l"(word)
+                   : "memory");
+    }
+  }
+  if ((int)threadIdx.x < grid) {
+    const unsigned long long* const p = slots + 4 * threadIdx.x;
+    unsigned long long w0, w1, w2, w3;
+    for (;;) {
+      asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+      asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w2), "=l"(w3) : "l"(p + 2) : "memory");
+      if ((unsigned)(w0 >> 32) == phase && (unsigned)(w1 >> 32) == phase &&
+          (unsigned)(w2 >> 32) == phase && (unsigned)(w3 >> 32) == phase)
+        break;
+      __nanosleep(40);
+    }
+    sh.gath[0][threadIdx.x] = __hiloint2double((int)(unsigned)w1, (int)(unsigned)w0);
+    sh.gath[1][threadIdx.x] = __hiloint2double((int)(unsigned)w3, (int)(unsigned)w2);
+  }
+  __syncthreads();
+  double ta = 0.0, tb = 0.0;
+  for (int k = lane; k < grid; k += 32) {
+    ta += sh.gath[0][k];
+    tb += sh.gath[1][k];
+  }
+  ta = warp_sum(ta);
+  tb = warp_sum(tb);
+  return make_double2(__shfl_sync(0xffffffffu, ta, 0), __shfl_sync(0xffffffffu, tb, 0));
 }
 
 __global__ void __launch_bounds__(kChainThreads, 1)
     k_mgs_chain(size_t n, size_t chunk, double* __restrict__ w, const double* const* __restrict__ v,
                 int last, double* dh, double* dnorm0, double* dnrmw, double* __restrict__ vout,
-                double* partials, unsigned int* bar) {
+                unsigned long long* flags) {
   extern __shared__ __align__(16) double ws[];  // this CTA's slice of w
-  __shared__ double red[2][kChainThreads / 32];
-  __shared__ double sums[2];
+  __shared__ ChainShared sh;
   const size_t lo = blockIdx.x * chunk;
   const int cnt = lo < n ? (int)((n - lo < chunk) ? n - lo : chunk) : 0;
   const uint64_t keep = policy_keep(), stream = policy_stream();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned phase = 0;
-  // grid-wide sums of (a, b): per-CTA partials (double-buffered by phase
-  // parity), one barrier, then every CTA adds them in CTA order
+  double2 sums;
   auto grid_sum = [&](double a, double b) {
-    a = warp_sum(a);
-    b = warp_sum(b);
-    if (lane == 0) {
-      red[0][warp] = a;
-      red[1][warp] = b;
-    }
-    __syncthreads();
-    double* const part = partials + (phase & 1) * 2 * gridDim.x;
-    if (warp == 0) {  // the 32 warp partials, shuffle tree (fixed order)
-      const double ta = warp_sum(red[0][lane]), tb = warp_sum(red[1][lane]);
-      if (lane == 0) {
-        part[2 * blockIdx.x] = ta;
-        part[2 * blockIdx.x + 1] = tb;
-      }
-    }
-    ++phase;
-    grid_barrier(bar, phase * gridDim.x);
-    if (warp == 0) {
-      double ta = 0.0, tb = 0.0;
-      for (int k = lane; k < (int)gridDim.x; k += 32) {
-        ta += __ldcg(part + 2 * k);
-        tb += __ldcg(part + 2 * k + 1);
-      }
-      ta = warp_sum(ta);
-      tb = warp_sum(tb);
-      if (lane == 0) {
-        sums[0] = ta;
-        sums[1] = tb;
-      }
-    }
-    __syncthreads();
+    sums = chain_grid_sum(a, b, sh, flags, phase);
   };
 
   // pairs of elements (16-byte loads; the slice start is even), plus the odd
@@ -448,8 +463,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     }
     grid_sum(a0, a1);
   }
-  const double norm0 = sqrt(sums[0]);
-  double h = sums[1];
+  const double norm0 = sqrt(sums.x);
+  double h = sums.y;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *dnorm0 = norm0;
     dh[0] = h;
@@ -461,7 +476,6 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     const double* vn = k < last ? v[k + 1] + lo : nullptr;
     const double nh = -h;
     double acc = 0.0;
-    __syncthreads();  // sums[] is rewritten by this pass's reduction
     if (vn) {
 #pragma unroll 4
       for (int e = threadIdx.x; e < pairs; e += kChainThreads) {
@@ -492,10 +506,10 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     }
     grid_sum(acc, 0.0);
     if (k < last) {
-      h = sums[0];
+      h = sums.x;
       if (blockIdx.x == 0 && threadIdx.x == 0) dh[k + 1] = h;
     } else {
-      hip = sqrt(sums[0]);
+      hip = sqrt(sums.x);
       if (blockIdx.x == 0 && threadIdx.x == 0) *dnrmw = hip;
     }
   }
@@ -537,17 +551,16 @@ constexpr int kChainSlots = 16;  // double2 per thread in tensor memory
 __global__ void __launch_bounds__(kChainThreads, 1)
     k_mgs_chain_tmem(size_t n, size_t chunk, double* __restrict__ w,
                      const double* const* __restrict__ v, int last, double* dh, double* dnorm0,
-                     double* dnrmw, double* __restrict__ vout, double* partials,
-                     unsigned int* bar) {
+                     double* dnrmw, double* __restrict__ vout,
+                     unsigned long long* flags) {
   extern __shared__ __align__(16) double vs[];  // this CTA's slice of the pass's basis vector
-  __shared__ double red[2][kChainThreads / 32];
-  __shared__ double sums[2];
+  __shared__ ChainShared sh;
   __shared__ uint32_t s_tbase;
   __shared__ double w_tail;  // the odd last element of the last slice
   const size_t lo = blockIdx.x * chunk;
   const int cnt = lo < n ? (int)((n - lo < chunk) ? n - lo : chunk) : 0;
   const uint64_t keep = policy_keep(), stream = policy_stream();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5;
   if (warp == 0) tmem_alloc<512>(&s_tbase);
   tmem_fence_before();
   __syncthreads();
@@ -555,38 +568,9 @@ __global__ void __launch_bounds__(kChainThreads, 1)
   const uint32_t tbase = s_tbase;
   const uint32_t tw = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 64);
   unsigned phase = 0;
+  double2 sums;
   auto grid_sum = [&](double a, double b) {
-    a = warp_sum(a);
-    b = warp_sum(b);
-    if (lane == 0) {
-      red[0][warp] = a;
-      red[1][warp] = b;
-    }
-    __syncthreads();
-    double* const part = partials + (phase & 1) * 2 * gridDim.x;
-    if (warp == 0) {  // the 32 warp partials, shuffle tree (fixed order)
-      const double ta = warp_sum(red[0][lane]), tb = warp_sum(red[1][lane]);
-      if (lane == 0) {
-        part[2 * blockIdx.x] = ta;
-        part[2 * blockIdx.x + 1] = tb;
-      }
-    }
-    ++phase;
-    grid_barrier(bar, phase * gridDim.x);
-    if (warp == 0) {
-      double ta = 0.0, tb = 0.0;
-      for (int k = lane; k < (int)gridDim.x; k += 32) {
-        ta += __ldcg(part + 2 * k);
-        tb += __ldcg(part + 2 * k + 1);
-      }
-      ta = warp_sum(ta);
-      tb = warp_sum(tb);
-      if (lane == 0) {
-        sums[0] = ta;
-        sums[1] = tb;
-      }
-    }
-    __syncthreads();
+    sums = chain_grid_sum(a, b, sh, flags, phase);
   };
   double2* const vs2 = reinterpret_cast<double2*>(vs);
   const int pairs = cnt >> 1, tail = (cnt & 1) ? cnt - 1 : -1;
@@ -671,8 +655,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     tmem_wait_st();
     grid_sum(a0, a1);
   }
-  const double norm0 = sqrt(sums[0]);
-  double h = sums[1];
+  const double norm0 = sqrt(sums.x);
+  double h = sums.y;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *dnorm0 = norm0;
     dh[0] = h;
@@ -686,7 +670,6 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     const double* vn = k < last ? v[k + 1] + lo : nullptr;
     const double nh = -h;
     double acc = 0.0;
-    __syncthreads();  // sums[] is rewritten by this pass's reduction
 #if FDE_CHAIN_ASYNC
     // Every pair of the slice belongs to one thread (shared-memory slot and
     // tensor-memory slot alike), so the thread that has subtracted h_k v_k[e]
@@ -789,10 +772,10 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     tmem_wait_st();
     grid_sum(acc, 0.0);
     if (k < last) {
-      h = sums[0];
+      h = sums.x;
       if (blockIdx.x == 0 && threadIdx.x == 0) dh[k + 1] = h;
     } else {
-      hip = sqrt(sums[0]);
+      hip = sqrt(sums.x);
       if (blockIdx.x == 0 && threadIdx.x == 0) *dnrmw = hip;
     }
   }
@@ -984,16 +967,16 @@ bool Reducer::mgs_chain(size_t n, double* w, const double* const* v_dev, int las
   });
   const int grid = su.grid;
   const size_t max_smem = su.max_smem;
-  if (grid == 0) return false;
+  if (grid == 0 || grid > kChainMaxGrid) return false;
   const size_t chunk = ((n + grid - 1) / grid + 1) & ~size_t(1);
   if (chunk * sizeof(double) > max_smem) return false;
   const bool in_tmem = FDE_CHAIN_TMEM && chunk >= FDE_CHAIN_TMEM_MIN &&
                        chunk <= 2 * (size_t)kChainSlots * kChainThreads;
-  if (chain_partials_.size() == 0) {
-    chain_partials_.alloc(4 * (size_t)grid);
-    chain_bar_.alloc(1);
+  if (chain_flags_.size() == 0) {
+    chain_flags_.alloc(8 * (size_t)grid);  // 2 epoch parities x 4 flag words per CTA
   }
-  FDE_CUDA(cudaMemsetAsync(chain_bar_.get(), 0, sizeof(unsigned int), s));
+  // epochs restart at 1 in every launch: clear the flag words
+  FDE_CUDA(cudaMemsetAsync(chain_flags_.get(), 0, 8 * (size_t)grid * sizeof(unsigned long long), s));
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
@@ -1006,7 +989,7 @@ bool Reducer::mgs_chain(size_t n, double* w, const double* const* v_dev, int las
   cfg.numAttrs = 1;
   cuda_check(cudaLaunchKernelEx(&cfg, in_tmem ? k_mgs_chain_tmem : k_mgs_chain, n, chunk, w, v_dev,
                                 last, dh, dnorm0, dnrmw,
-                                vout, chain_partials_.get(), chain_bar_.get()),
+                                vout, chain_flags_.get()),
              "kernel launch");
   FDE_LAUNCH_CHECK();
   return true;

@@ -86,8 +86,7 @@ class Reducer {
  private:
   DevBuf<double> partials_;
   DevBuf<unsigned int> counter_;
-  DevBuf<double> chain_partials_;
-  DevBuf<unsigned int> chain_bar_;
+  DevBuf<unsigned long long> chain_flags_;  // flag-carrying partial sums of the chain's reductions
 };
 
 Xfer make_xfer(int n1, int n2, bool cx, bool cy);

@@ -371,24 +371,26 @@ struct ChainShared {
   double red[2][kChainThreads / 32];
   double gath[2][kChainMaxGrid];
 };
+// TWO = false: only a is summed (b's words are neither written nor polled)
+template <bool TWO>
 __device__ __forceinline__ double2 chain_grid_sum(double a, double b, ChainShared& sh,
                                                   unsigned long long* ll, unsigned& phase) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grid = (int)gridDim.x;
   a = warp_sum(a);
-  b = warp_sum(b);
+  if (TWO) b = warp_sum(b);
   if (lane == 0) {
     sh.red[0][warp] = a;
-    sh.red[1][warp] = b;
+    if (TWO) sh.red[1][warp] = b;
   }
   __syncthreads();
   ++phase;
   unsigned long long* const slots = ll + (size_t)(phase & 1) * 4 * grid;
   if (warp == 0) {  // the 32 warp partials, shuffle tree (fixed order)
-    double ta = warp_sum(sh.red[0][lane]), tb = warp_sum(sh.red[1][lane]);
+    double ta = warp_sum(sh.red[0][lane]), tb = TWO ? warp_sum(sh.red[1][lane]) : 0.0;
     ta = __shfl_sync(0xffffffffu, ta, 0);
-    tb = __shfl_sync(0xffffffffu, tb, 0);
-    if (lane < 4) {
+    if (TWO) tb = __shfl_sync(0xffffffffu, tb, 0);
+    if (lane < (TWO ? 4 : 2)) {
       const double val = lane < 2 ? ta : tb;
       const unsigned half = (lane & 1) ? (unsigned)__double2hiint(val) : (unsigned)__double2loint(val);
       const unsigned long long word = ((unsigned long long)phase << 32) | half;
@@ -399,27 +401,28 @@ __device__ __forceinline__ double2 chain_grid_sum(double a, double b, ChainShare
   }
   if ((int)threadIdx.x < grid) {
     const unsigned long long* const p = slots + 4 * threadIdx.x;
-    unsigned long long w0, w1, w2, w3;
+    unsigned long long w0, w1, w2 = 0, w3 = 0;
     for (;;) {
       asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
-      asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w2), "=l"(w3) : "l"(p + 2) : "memory");
+      if (TWO)
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w2), "=l"(w3) : "l"(p + 2) : "memory");
       if ((unsigned)(w0 >> 32) == phase && (unsigned)(w1 >> 32) == phase &&
-          (unsigned)(w2 >> 32) == phase && (unsigned)(w3 >> 32) == phase)
+          (!TWO || ((unsigned)(w2 >> 32) == phase && (unsigned)(w3 >> 32) == phase)))
         break;
-      __nanosleep(40);
+      __nanosleep(40);  // (200 / 1000 ns measured: 8.5 / 8.7 us per projection against 8.2)
     }
     sh.gath[0][threadIdx.x] = __hiloint2double((int)(unsigned)w1, (int)(unsigned)w0);
-    sh.gath[1][threadIdx.x] = __hiloint2double((int)(unsigned)w3, (int)(unsigned)w2);
+    if (TWO) sh.gath[1][threadIdx.x] = __hiloint2double((int)(unsigned)w3, (int)(unsigned)w2);
   }
   __syncthreads();
   double ta = 0.0, tb = 0.0;
   for (int k = lane; k < grid; k += 32) {
     ta += sh.gath[0][k];
-    tb += sh.gath[1][k];
+    if (TWO) tb += sh.gath[1][k];
   }
   ta = warp_sum(ta);
-  tb = warp_sum(tb);
-  return make_double2(__shfl_sync(0xffffffffu, ta, 0), __shfl_sync(0xffffffffu, tb, 0));
+  if (TWO) tb = warp_sum(tb);
+  return make_double2(__shfl_sync(0xffffffffu, ta, 0), TWO ? __shfl_sync(0xffffffffu, tb, 0) : 0.0);
 }
 
 __global__ void __launch_bounds__(kChainThreads, 1)
@@ -433,9 +436,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
   const uint64_t keep = policy_keep(), stream = policy_stream();
   unsigned phase = 0;
   double2 sums;
-  auto grid_sum = [&](double a, double b) {
-    sums = chain_grid_sum(a, b, sh, flags, phase);
-  };
+  auto grid_sum = [&](double a, double b) { sums = chain_grid_sum<true>(a, b, sh, flags, phase); };
+  auto grid_sum1 = [&](double a) { sums = chain_grid_sum<false>(a, 0.0, sh, flags, phase); };
 
   // pairs of elements (16-byte loads; the slice start is even), plus the odd
   // last element of the last slice
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
       ws[tail] = wi;
       acc = fma(vn ? vn[tail] : wi, wi, acc);
     }
-    grid_sum(acc, 0.0);
+    grid_sum1(acc);
     if (k < last) {
       h = sums.x;
       if (blockIdx.x == 0 && threadIdx.x == 0) dh[k + 1] = h;
@@ -542,6 +544,10 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 constexpr int kChainSlots = 16;  // double2 per thread in tensor memory
 #ifndef FDE_CHAIN_ASYNC
 #define FDE_CHAIN_ASYNC 1  // v_{k+1} by per-thread asynchronous copies into its shared-memory slots
+// (measured: each 16-byte cp.async.cg fetches its whole 32-byte sector, so a pass moves 68 MB L2 -> SM
+// for a 33.5 MB vector; .ca halves that and runs 10.2 us per projection against 8.5; one 512-byte bulk
+// copy per warp and slot with an mbarrier per slot group also halves it and runs 8.9 -- the pass is no
+// longer bound by that path, the per-thread .cg copies stay)
 #endif
 #ifndef FDE_CHAIN_LOADS
 #define FDE_CHAIN_LOADS 4  // 16-byte loads of v_{k+1} in flight per thread; 8 / 16 spill at 64 registers: 10.3 -> 13.1 / 14.5 us per pass
@@ -569,9 +575,8 @@ __global__ void __launch_bounds__(kChainThreads, 1)
   const uint32_t tw = tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((warp >> 2) * 64);
   unsigned phase = 0;
   double2 sums;
-  auto grid_sum = [&](double a, double b) {
-    sums = chain_grid_sum(a, b, sh, flags, phase);
-  };
+  auto grid_sum = [&](double a, double b) { sums = chain_grid_sum<true>(a, b, sh, flags, phase); };
+  auto grid_sum1 = [&](double a) { sums = chain_grid_sum<false>(a, 0.0, sh, flags, phase); };
   double2* const vs2 = reinterpret_cast<double2*>(vs);
   const int pairs = cnt >> 1, tail = (cnt & 1) ? cnt - 1 : -1;
   // ||w|| and <w, v_0>: w moves into tensor memory, v_0 into shared memory
@@ -770,7 +775,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
       acc = fma(vn ? vn[tail] : wi, wi, acc);
     }
     tmem_wait_st();
-    grid_sum(acc, 0.0);
+    grid_sum1(acc);
     if (k < last) {
       h = sums.x;
       if (blockIdx.x == 0 && threadIdx.x == 0) dh[k + 1] = h;

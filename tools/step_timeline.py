@@ -1,4 +1,4 @@
-"""Kernel timeline of cfg4 time steps (CUPTI via torch.profiler): total span,
+"""Kernel timeline of cfg4 (or argv[2]) time steps (CUPTI via torch.profiler): total span,
 sum of kernel durations, gaps, and the per-kernel-family totals."""
 import sys
 from collections import defaultdict
@@ -10,8 +10,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_1706_06844_b200 as fde
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-p = fde.Problem.preset_config(4, steps=8)
-cfg = fde.DriverConfig(precond=fde.PRECOND_MGM, tol=1e-8, restart=20, max_outer=100, omega=0.7,
+cfg_id = int(sys.argv[2]) if len(sys.argv) > 2 else 4  # BASELINE config (3: GMRES(30))
+p = fde.Problem.preset_config(cfg_id, steps=8)
+cfg = fde.DriverConfig(precond=fde.PRECOND_MGM, tol=1e-8, restart=30 if cfg_id == 3 else 20, max_outer=100, omega=0.7,
                        cycles=1, coarse=fde.COARSE_SWEEPS, coarse_sweeps=3)
 m = fde.March(p, p.n, p.n, 8, cfg)
 for _ in range(2):

@@ -612,7 +612,10 @@ struct PairedShape {
 };
 
 #ifndef FDE_P8_Y10
-#define FDE_P8_Y10 0  // column passes at M = 1024 with 8 points/thread (one line per CTA): measured no change
+#define FDE_P8_Y10 0  // every column pass at M = 1024 with 8 points/thread (one line per CTA): cfg4 +0.5 %, but the n = 1023 apply 42 -> 48 us (1023 CTAs: two waves)
+#endif
+#ifndef FDE_P8_Y10_WAVE
+#define FDE_P8_Y10_WAVE 1  // ... only when its lines fit one wave of resident CTAs (cfg4's 511-column levels): V-cycle 621.0 -> 616.4 us
 #endif
 #ifndef FDE_TMEM_LD64
 #define FDE_TMEM_LD64 1  // one 32x32b.x64 load + wait per spectrum (measured +0.1 %)
@@ -1028,21 +1031,26 @@ template <int LOGM>
 constexpr int paired_pts_for(bool ypass) {
   return LOGM == 8 || (LOGM == 10 && (!FDE_P16_M1024 || (ypass && FDE_P8_Y10))) ? 8 : 16;
 }
-template <int LOGM, class Pol>
-constexpr int paired_pts() { return paired_pts_for<LOGM>(std::is_same<Pol, YPass>::value); }
+// P8: the 8-point instance of a column pass at M = 1024, chosen at launch
+template <int LOGM, class Pol, bool P8 = false>
+constexpr int paired_pts() {
+  return (P8 && LOGM == 10 && std::is_same<Pol, YPass>::value)
+             ? 8
+             : paired_pts_for<LOGM>(std::is_same<Pol, YPass>::value);
+}
 
-template <int LOGM, class Pol, int EPI>
+template <int LOGM, class Pol, int EPI, bool P8 = false>
 #ifndef FDE_STAGGER_Y_NS
 #define FDE_STAGGER_Y_NS 0
 #endif
 #ifndef FDE_PAIRED_CTAS
 #define FDE_PAIRED_CTAS 4  // resident 128-thread CTAs per SM the register budget is cut for
 #endif
-__global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CTA_THREADS,
-                                  FDE_PAIRED_CTAS * 128 / PairedShape<LOGM, paired_pts<LOGM, Pol>()>::CTA_THREADS)
+__global__ void __launch_bounds__(PairedShape<LOGM, paired_pts<LOGM, Pol, P8>()>::CTA_THREADS,
+                                  FDE_PAIRED_CTAS * 128 / PairedShape<LOGM, paired_pts<LOGM, Pol, P8>()>::CTA_THREADS)
     fft_line_kernel_paired(const Pol p) {
   const bool late_wait = pass_enter(p);
-  constexpr int P = paired_pts<LOGM, Pol>();
+  constexpr int P = paired_pts<LOGM, Pol, P8>();
   using S = PairedShape<LOGM, P>;
   using IO = LineIO<Pol, EPI>;
   constexpr int T = S::T, H = P / 2, R0 = S::R0, B0 = S::B0, NS0 = S::NS0;
@@ -1467,9 +1475,9 @@ inline int paired_parity(const YPass& p) {
   return common_parity({p.x, p.epT, p.emT, p.qT ? p.q : nullptr});
 }
 
-template <int LOGM, class P, int EPI>
+template <int LOGM, class P, int EPI, bool P8 = false>
 bool launch_paired_epi(const P& p, cudaStream_t s) {
-  constexpr int PP = paired_pts<LOGM, P>();
+  constexpr int PP = paired_pts<LOGM, P, P8>();
   using S = PairedShape<LOGM, PP>;
   // resident CTAs on the device (persistent grid) and the shared-memory
   // carveout that just holds them: registers, tensor-memory columns and
@@ -1484,10 +1492,10 @@ bool launch_paired_epi(const P& p, cudaStream_t s) {
     FDE_CUDA(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
     FDE_CUDA(cudaDeviceGetAttribute(&smem_rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev));
     FDE_CUDA(cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev));
-    FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
+    FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI, P8>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
     cudaFuncAttributes fa{};
-    FDE_CUDA(cudaFuncGetAttributes(&fa, fft_line_kernel_paired<LOGM, P, EPI>));
+    FDE_CUDA(cudaFuncGetAttributes(&fa, fft_line_kernel_paired<LOGM, P, EPI, P8>));
     const int regs_cta = ((fa.numRegs * 32 + 255) / 256 * 256) * (S::CTA_THREADS / 32);
     const int cta_smem = (int)(S::SMEM + fa.sharedSizeBytes) + smem_rsv;
     int per_sm = regs_sm / regs_cta;
@@ -1498,13 +1506,13 @@ bool launch_paired_epi(const P& p, cudaStream_t s) {
     if (per_sm < 1) per_sm = 1;
     int carve = (per_sm * cta_smem * 100 + smem_sm - 1) / smem_sm + FDE_PAIRED_CARVEOUT_PAD;
     if (carve > 100) carve = 100;
-    FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI>,
+    FDE_CUDA(cudaFuncSetAttribute(fft_line_kernel_paired<LOGM, P, EPI, P8>,
                                   cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     return sms * per_sm;
   });
   const int groups = (lines_of(p) + S::LPC - 1) / S::LPC;
   const int ctas = (groups + S::NG - 1) / S::NG;
-  launch_k(fft_line_kernel_paired<LOGM, P, EPI>, ctas < max_ctas ? ctas : max_ctas,
+  launch_k(fft_line_kernel_paired<LOGM, P, EPI, P8>, ctas < max_ctas ? ctas : max_ctas,
            S::CTA_THREADS, S::SMEM, s, p);
   FDE_LAUNCH_CHECK();
   return true;
@@ -1516,6 +1524,20 @@ bool launch_paired(const P& p0, cudaStream_t s) {
   p.par = paired_parity(p);
   if (p.par < 0 || p.blk.n + 1 > (1 << LOGM)) return launch_fft<LOGM>(p0, s);
   if constexpr (std::is_same<P, YPass>::value) {
+    if constexpr (LOGM == 10 && FDE_P8_Y10_WAVE && paired_pts<LOGM, P>() == 16) {
+      // few enough columns for one wave of resident CTAs (4 per SM): one
+      // line per CTA with 8 points per thread halves the serial chain
+      static DeviceCache<int> wave;
+      const int one_wave = wave.get([](int dev) {
+        int sms = 0;
+        FDE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        return FDE_PAIRED_CTAS * sms;
+      });
+      if (lines_of(p) <= one_wave) {
+        if (p.qT) return launch_paired_epi<LOGM, P, 2, true>(p, s);
+        return launch_paired_epi<LOGM, P, 0, true>(p, s);
+      }
+    }
     if (p.qT) return launch_paired_epi<LOGM, P, 2>(p, s);
     return launch_paired_epi<LOGM, P, 0>(p, s);
   } else {

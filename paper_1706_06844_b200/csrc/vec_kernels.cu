@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
       cp_async_commit();
     }
 #pragma unroll 1  // (unrolled, the loads of every round are hoisted and spill)
-    for (int g = 0; g < kChainSlots; g += 4) {
+    for (int g = 0; g < kChainSlots && g * kChainThreads < pairs; g += 4) {  // (live slot groups only)
       double2 wv[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -615,6 +615,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 #pragma unroll
     for (int g = 0; g < kChainSlots; g += 4) {
       cp_async_wait_group_le(3 - g / 4);
+      if (g * kChainThreads >= pairs) continue;  // short slices: the slot group is empty in every thread
       double2 wv[4];
       tmem_ld4(tw + 4 * g, wv);
 #pragma unroll
@@ -684,6 +685,10 @@ __global__ void __launch_bounds__(kChainThreads, 1)
     // the same slot order as the fused walk: identical bits.
 #pragma unroll
     for (int g = 0; g < kChainSlots; g += 4) {
+      if (g * kChainThreads >= pairs) {  // empty slot group (uniform over the CTA)
+        if (vn) cp_async_commit();       // keeps the group count the waits below assume
+        continue;
+      }
       double2 wv[4];
       tmem_ld4(tw + 4 * g, wv);
 #pragma unroll
@@ -716,6 +721,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 #pragma unroll
       for (int g = 0; g < kChainSlots; g += 4) {
         cp_async_wait_group_le(3 - g / 4);
+        if (g * kChainThreads >= pairs) continue;
         double2 wv[4];
         tmem_ld4(tw + 4 * g, wv);
 #pragma unroll
@@ -791,6 +797,7 @@ __global__ void __launch_bounds__(kChainThreads, 1)
   double2* const out2 = reinterpret_cast<double2*>((keep_w ? w : vout) + lo);
 #pragma unroll
   for (int g = 0; g < kChainSlots; g += 4) {
+    if (g * kChainThreads >= pairs) continue;
     double2 wv[4];
     tmem_ld4(tw + 4 * g, wv);
 #pragma unroll

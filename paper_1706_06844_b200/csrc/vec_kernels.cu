@@ -385,6 +385,13 @@ __device__ __forceinline__ double2 chain_grid_sum(double a, double b, ChainShare
   }
   __syncthreads();
   ++phase;
+  if (grid == 1) {  // a single CTA: the warp partials are the whole sum, nothing leaves the SM
+    double ta = warp_sum(sh.red[0][lane]), tb = TWO ? warp_sum(sh.red[1][lane]) : 0.0;
+    ta = __shfl_sync(0xffffffffu, ta, 0);
+    if (TWO) tb = __shfl_sync(0xffffffffu, tb, 0);
+    __syncthreads();  // sh.red is rewritten by the next reduction
+    return make_double2(ta, tb);
+  }
   unsigned long long* const slots = ll + (size_t)(phase & 1) * 4 * grid;
   if (warp == 0) {  // the 32 warp partials, shuffle tree (fixed order)
     double ta = warp_sum(sh.red[0][lane]), tb = TWO ? warp_sum(sh.red[1][lane]) : 0.0;
@@ -819,6 +826,9 @@ __global__ void __launch_bounds__(kChainThreads, 1)
 // slices from this many doubles per SM up run the tensor-memory chain; below,
 // the allocation and the fixed 16-slot walk cost more than the second L2
 // stream (cfg1 894 -> 808, cfg2 650 -> 611 steps/s with it)
+#ifndef FDE_CHAIN_MIN_SLICE
+#define FDE_CHAIN_MIN_SLICE 4096  // doubles per CTA below which the chain runs on fewer CTAs than SMs (0: always one per SM)
+#endif
 #ifndef FDE_CHAIN_TMEM_MIN
 #define FDE_CHAIN_TMEM_MIN 4096
 #endif
@@ -977,15 +987,23 @@ bool Reducer::mgs_chain(size_t n, double* w, const double* const* v_dev, int las
     }
     return r;
   });
-  const int grid = su.grid;
   const size_t max_smem = su.max_smem;
-  if (grid == 0 || grid > kChainMaxGrid) return false;
+  if (su.grid == 0 || su.grid > kChainMaxGrid) return false;
+  // short vectors: one CTA per FDE_CHAIN_MIN_SLICE doubles instead of one per
+  // SM (cfg1's 3969 unknowns: a single CTA, whose reductions never leave it)
+  int grid = su.grid;
+#if FDE_CHAIN_MIN_SLICE > 0
+  {
+    const size_t want = (n + FDE_CHAIN_MIN_SLICE - 1) / FDE_CHAIN_MIN_SLICE;
+    if (want < (size_t)grid) grid = want < 1 ? 1 : (int)want;
+  }
+#endif
   const size_t chunk = ((n + grid - 1) / grid + 1) & ~size_t(1);
   if (chunk * sizeof(double) > max_smem) return false;
   const bool in_tmem = FDE_CHAIN_TMEM && chunk >= FDE_CHAIN_TMEM_MIN &&
                        chunk <= 2 * (size_t)kChainSlots * kChainThreads;
   if (chain_flags_.size() == 0) {
-    chain_flags_.alloc(8 * (size_t)grid);  // 2 epoch parities x 4 flag words per CTA
+    chain_flags_.alloc(8 * (size_t)su.grid);  // 2 epoch parities x 4 flag words per CTA
   }
   // epochs restart at 1 in every launch: clear the flag words
   FDE_CUDA(cudaMemsetAsync(chain_flags_.get(), 0, 8 * (size_t)grid * sizeof(unsigned long long), s));
